@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark of batched HDC inference (ScalableHD hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--prec fp32]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+    python bench.py --impl reference ...                    (the CPU oracle arm)
+
+A step = one hdc_model_infer call over one batch of the configuration (all of
+Alg. 1: encode, HardSign, similarity, argmax), inputs resident in HBM.  Multi-GPU
+runs are weak-scaling: every rank infers its own batch of the configuration
+(rows r*N..(r+1)*N of the generator stream); there is no data-path collective.
+Prints ONE JSON line (rank 0).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                  "sm_max_mhz": 1965.0}
+N_SM = 148
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--prec", default="fp32", choices=["fp32", "tf32", "bf16", "fp32_tc"])
+    ap.add_argument("--path", default="auto", choices=["auto", "small", "fused"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+            except ValueError:
+                continue
+            for i, n in enumerate(names):
+                if s[3 + i].lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_rate(cfg, seconds, nthreads=0, max_rows=None):
+    """Time the CPU oracle (as it stands) on a bounded row sample of `cfg`."""
+    import oracle
+    from hdc_inputs import make_B, make_C, make_X
+    B, C = make_B(cfg), make_C(cfg)
+    threads = oracle.num_threads() if nthreads <= 0 else nthreads
+    probe = min(cfg.N, max(1, threads))
+    X = make_X(cfg, 0, probe)
+    t0 = time.perf_counter()
+    oracle.infer(X, B, C, nthreads=threads)
+    dt = time.perf_counter() - t0
+    rows = int(max(probe, min(cfg.N, probe * seconds / max(dt, 1e-6))))
+    if max_rows:
+        rows = min(rows, max_rows)
+    X = make_X(cfg, 0, rows)
+    t0 = time.perf_counter()
+    oracle.infer(X, B, C, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return rows / dt, rows, dt, threads, (B, C)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    from hdc_inputs import CONFIGS, make_B, make_C, make_X
+    import oracle
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    B, C = make_B(cfg), make_C(cfg)
+    threads = oracle.num_threads()
+    # size each step's row sample so the whole run stays within ~2-3 minutes
+    probe = max(1, threads)
+    t0 = time.perf_counter()
+    oracle.infer(make_X(cfg, 0, probe), B, C, nthreads=threads)
+    per_row = (time.perf_counter() - t0) / probe
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    rows = int(max(1, min(cfg.N, budget / max(per_row, 1e-9))))
+    X = make_X(cfg, 0, rows)
+    for _ in range(args.warmup):
+        oracle.infer(X, B, C, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.infer(X, B, C, nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = rows * args.steps / dt
+    sample = "%d of %d rows of %s per step (rows are independent)" % (rows, cfg.N, cfg.name)
+    out = {"impl": "reference", "metric": "samples_per_s", "value": value, "unit": "samples/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
+                      "sample_rows": rows},
+           "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "oracle",
+                            "sample": sample, "cpu": cpu_model()},
+           "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
+    N, F, D, K = cfg.N, cfg.F, cfg.D, cfg.K
+    flops = 2.0 * N * F * D + 2.0 * N * D * K
+    bytes_ = 4.0 * D * (F + K) + 4.0 * N * F + 4.0 * N
+    small = (path == "small") or (path == "auto" and N <= 32)
+    if small:
+        achieved = bytes_ / (ms_kernel * 1e-3) / 1e9
+        peak = float(peaks["hbm_gbs"])
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "algorithmic_per_launch": bytes_}
+    achieved = flops / (ms_kernel * 1e-3) / 1e12
+    if prec == "fp32":
+        mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = N_SM * 128 * 2 * mhz * 1e6 / 1e12       # FFMA: 148 SM x 128 lanes x 2 flop
+        bound = "alu"
+    else:
+        bf16 = float(peaks["bf16_tflops"])
+        peak = bf16 / 2.0 if prec == "tf32" else bf16  # tf32 dense = 1/2 bf16 (nominal ratio)
+        bound = "tensor"
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": flops}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from hdc_inputs import CONFIGS, make_B, make_C
+    from hdc_inputs.device import make_X_device
+    import paper_2506_09282_b200 as hdc
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS[args.config]
+    peaks, peaks_src = load_peaks()
+    B = torch.from_numpy(make_B(cfg)).to(dev)
+    C = torch.from_numpy(make_C(cfg)).to(dev)
+    # weak scaling: rank r infers rows [r N, (r+1) N) of the X stream
+    X = make_X_device(cfg, dev, rank * cfg.N, (rank + 1) * cfg.N)
+    model = hdc.Model(B, C, prec=args.prec)
+    labels = torch.empty(cfg.N, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        model.infer(X, labels=labels, path=args.path)
+    torch.cuda.synchronize()
+    launches_per_step = model.last_launch_count()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.fill_(float(i))                          # evict X, B, C from L2 (untimed)
+        starts[i].record(stream)
+        model.infer(X, labels=labels, path=args.path)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = cfg.N * world * args.steps / (total_ms * 1e-3)
+
+    # end to end through the public host-buffer entry point (H2D X, D2H labels)
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        yh = torch.empty(cfg.N, dtype=torch.int32).pin_memory()
+        for _ in range(2):
+            model.infer_host(Xh, yh)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            model.infer_host(Xh, yh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.N * world * args.steps / (float(te.item()) * 1e-3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4)}
+
+    if rank != 0:
+        return
+    roof = roofline_for(cfg, args.prec, args.path, ms_per_step / max(1, launches_per_step)
+                        if launches_per_step > 1 and cfg.N <= 32 else ms_per_step, peaks, clk["sm_mhz"])
+    roof["peak_source"] = peaks_src
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, rows, dt, threads, _ = oracle_rate(cfg, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",
+               "sample": "first %d of %d rows of %s (%.1f s, rows independent)" % (rows, cfg.N, cfg.name, dt),
+               "cpu": cpu_model()}
+    out = {"metric": "samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16", "fp32_tc": "bf16x3"}[args.prec],
+           "data": "synthetic",
+           "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
+                      "prec": args.prec, "path": args.path, "global_batch": cfg.N * world,
+                      "l2": "flushed between steps (write of 2x L2 bytes, untimed)",
+                      "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": launches_per_step * args.steps, "clocks": clk,
+           "ms_per_step_min": min(ms), "ms_per_step_median": sorted(ms)[len(ms) // 2]}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * hdc.h -- C ABI of libhdc.so: batched HDC inference on B200 (sm_100a).
+ *
+ * The operation (ScalableHD, arXiv 2506.09282; PAPER.md line numbers "P:n"):
+ *   Alg. 1 "Two-Stage HDC Inference", batch form P:171-190:
+ *     Stage I    H = HardSign(X B)        eq. batch_encode
+ *                HardSign(v) = +1 if v >= 0 else -1   eq. hardsign
+ *     Stage II   S = H C^T                eq. batch_sim
+ *                y = argmax_k S[n, k]     eq. pred_batch
+ *   with X (N x F), B (F x D, the base HVs), C (K x D, the paper's class matrix M).
+ *   Ties in the argmax go to the LOWEST class index (the paper is silent;
+ *   DESIGN.md reading R2).  HardSign(-0.0) = +1 (reading R1).
+ *
+ * Conventions for every entry point:
+ *   - All matrices are row-major, fp32, and DEVICE pointers unless the name says
+ *     _host.  They are caller-owned; the library never frees or retains them
+ *     beyond the call (hdc_model_create copies B and C into its own layout).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream) and return after enqueue, except hdc_model_create /
+ *     hdc_model_destroy which synchronise the device.
+ *   - Synchronous argument errors return HDC_ERR_INVALID_VALUE (bad sizes, NULL
+ *     required pointer, K > HDC_MAX_K) or HDC_ERR_MISALIGNED (pointer not 4-byte
+ *     aligned; labels 4-byte).  Asynchronous device faults surface as
+ *     HDC_ERR_CUDA on the next call (cuBLAS convention).
+ *   - Non-finite inputs are not checked on the hot path; outputs are then
+ *     unspecified.
+ *   - Determinism: the same inputs, precision and path give bit-identical
+ *     scores and labels (fixed-order reductions, no floating-point atomics).
+ *   - A model handle is immutable after creation but owns a workspace: calls on
+ *     ONE handle must be serialised (one stream at a time); use one handle per
+ *     concurrent stream.
+ */
+#ifndef HDC_H_
+#define HDC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDC_MAX_K 256
+
+typedef enum {
+  HDC_OK = 0,
+  HDC_ERR_INVALID_VALUE = 1,
+  HDC_ERR_MISALIGNED = 2,
+  HDC_ERR_UNSUPPORTED = 3,
+  HDC_ERR_NO_MEMORY = 4,
+  HDC_ERR_CUDA = 5
+} hdc_status_t;
+
+/* Arithmetic of Stage I.  The paper keeps B and M in fp32.
+ *   HDC_PREC_FP32: fp32 FFMA accumulation + float64 re-evaluation of every
+ *     pre-activation whose |v| is within the rigorous fp32 error bound
+ *     (F+32) 2^-24 ||x_n|| ||b_d||, so each HardSign decision equals the one
+ *     of the exact product X B (DESIGN.md §4 "sign recheck").
+ *   HDC_PREC_TF32 / HDC_PREC_BF16: Stage I on tcgen05 tensor cores with X and B
+ *     rounded to tf32 / bf16, fp32 accumulation; no recheck (approximate H).
+ *   HDC_PREC_FP32_TC: Stage I on tcgen05 as 3 bf16 products (hi*hi + lo*hi +
+ *     hi*lo) + the same float64 recheck, bound widened for the split error. */
+typedef enum {
+  HDC_PREC_FP32 = 0,
+  HDC_PREC_TF32 = 1,
+  HDC_PREC_BF16 = 2,
+  HDC_PREC_FP32_TC = 3
+} hdc_precision_t;
+
+/* Kernel selection (diagnostics and tests; HDC_PATH_AUTO is the product path).
+ *   SMALL: bandwidth-bound D-split kernel (streams B and C once per 32 rows).
+ *   FUSED: large-batch fused kernel (H never leaves the chip). */
+typedef enum { HDC_PATH_AUTO = 0, HDC_PATH_SMALL = 1, HDC_PATH_FUSED = 2 } hdc_path_t;
+
+typedef struct hdc_model_s* hdc_model_t;
+
+/* One-shot inference (BASELINE north_star "hdc_infer(X, B, C, N, F, D, K) ->
+ * labels plus optional scores").  Builds a temporary model (copies B, C),
+ * runs, and releases it; the copies and allocations are inside the call, which
+ * therefore synchronises the device (like hdc_model_create/destroy).
+ *   X [N*F], B [F*D], C [K*D]: inputs.   N >= 0, F >= 1, D >= 1, 1 <= K <= 256.
+ *   labels [N] int32 (required when N > 0): y_pred, values in [0, K).
+ *   scores [N*K] fp32 (nullable): S. */
+hdc_status_t hdc_infer(const float* X, const float* B, const float* C, int64_t N, int64_t F,
+                       int64_t D, int64_t K, int32_t* labels, float* scores,
+                       hdc_precision_t prec, void* stream);
+
+/* Amortised setup: copies B and C (device pointers) into the model's padded
+ * layouts and precomputes per-column norms ||b_d|| (sign recheck) and any
+ * low-precision operand copies `prec` needs.  Timed latency excludes this, as
+ * the paper's pre-tiled B and J.  Synchronises the device. */
+hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t D, int64_t K,
+                              hdc_precision_t prec, hdc_model_t* out);
+
+/* Inference on a resident model.  X [N*F] device; labels [N]; scores [N*K] or NULL. */
+hdc_status_t hdc_model_infer(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                             float* scores, void* stream);
+
+/* Same, with an explicit kernel path (see hdc_path_t). */
+hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                                  float* scores, hdc_path_t path, void* stream);
+
+/* End-to-end variant on HOST buffers: copies X_host (N*F fp32) to the device,
+ * runs hdc_model_infer, copies labels (and scores if non-NULL) back.  Host
+ * buffers should be pinned (cudaHostAlloc) for the copies to be asynchronous;
+ * the call returns after enqueue -- synchronise `stream` before reading them. */
+hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
+                                  int32_t* labels_host, float* scores_host, void* stream);
+
+/* D-shard piece (Alg. 3's per-worker S_local over its D column blocks):
+ * the model holds this rank's D-slice of B and C; writes the partial scores
+ * S_partial [N*K] = HardSign(X B_r) C_r^T (no argmax).  The caller sums the
+ * partials over ranks (Alg. 3 line `S += S_local`) and calls hdc_argmax. */
+hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, float* S_partial,
+                                      void* stream);
+
+/* Row argmax, lowest index among equal maxima: labels[n] = argmax_k S[n*K+k]. */
+hdc_status_t hdc_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, void* stream);
+
+/* Releases the model and its device memory.  Synchronises the device. */
+hdc_status_t hdc_model_destroy(hdc_model_t m);
+
+/* Model dimensions (any out pointer may be NULL). */
+hdc_status_t hdc_model_dims(hdc_model_t m, int64_t* F, int64_t* D, int64_t* K,
+                            hdc_precision_t* prec);
+
+/* Cumulative number of float64 sign re-evaluations performed by all calls on
+ * this model since creation; synchronises the device (diagnostic; -1 on error). */
+int64_t hdc_model_recheck_count(hdc_model_t m);
+
+/* Number of kernel launches the last call on this model enqueued. */
+int32_t hdc_model_last_launch_count(hdc_model_t m);
+
+const char* hdc_status_string(hdc_status_t st);
+/* Detail for the last failing call on this thread (thread-local, never NULL). */
+const char* hdc_last_error(void);
+/* Library version string. */
+const char* hdc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDC_H_ */

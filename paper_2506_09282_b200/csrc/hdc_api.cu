@@ -1,0 +1,320 @@
+// hdc_api.cu -- the C ABI of libhdc.so (include/hdc.h): validation, model
+// handles (padded operand layouts, norms), workspaces and kernel dispatch.
+//
+// Dispatch (the analogue of the paper's S/L variant choice by batch size,
+// P:222): N <= 32 -> K2 small-batch D-split kernel; larger N ->
+// the fused large-batch kernel (FFMA fp32-exact or tcgen05 by precision).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hdc.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace hdc;
+
+namespace {
+
+thread_local std::string g_last_error = "";
+
+hdc_status_t fail(hdc_status_t st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+hdc_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(HDC_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define HDC_CUDA_TRY(expr, where)                   \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+constexpr int64_t kMaxF = int64_t(1) << 20;
+constexpr int kSmallMaxN = 32;
+
+}  // namespace
+
+struct hdc_model_s {
+  int device = 0;
+  int64_t F = 0, D = 0, K = 0, Dp = 0;
+  hdc_precision_t prec = HDC_PREC_FP32;
+  float* Bp = nullptr;
+  float* Cp = nullptr;
+  float* bnorm = nullptr;
+  // small-batch workspace
+  float* S_part = nullptr;
+  float* S_grp = nullptr;
+  unsigned* cnt = nullptr;  // [G1 + 1]
+  unsigned long long* recheck = nullptr;
+  // host-buffer (e2e) staging, grown on demand
+  float* Xdev = nullptr;
+  int64_t Xdev_rows = 0;
+  int32_t* ldev = nullptr;
+  float* sdev = nullptr;
+  int32_t last_launches = 0;
+
+  ModelView view() const {
+    ModelView v;
+    v.F = F;
+    v.D = D;
+    v.K = K;
+    v.Dp = Dp;
+    v.Bp = Bp;
+    v.Cp = Cp;
+    v.bnorm = bnorm;
+    v.tau_coef = sign_bound_coef(F);
+    return v;
+  }
+  SmallWorkspace small_ws() const {
+    SmallWorkspace w;
+    w.S_part = S_part;
+    w.S_grp = S_grp;
+    w.cnt1 = cnt;
+    w.cnt2 = cnt + small_num_groups(D);
+    w.recheck = recheck;
+    return w;
+  }
+};
+
+namespace {
+
+hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
+  if (F < 1 || D < 1 || K < 1) return fail(HDC_ERR_INVALID_VALUE, "F, D, K must be >= 1");
+  if (K > HDC_MAX_K) return fail(HDC_ERR_INVALID_VALUE, "K > HDC_MAX_K (256)");
+  if (F > kMaxF) return fail(HDC_ERR_UNSUPPORTED, "F > 2^20 (sign-recheck bound validity)");
+  if (D > (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "D > 2^31");
+  return HDC_OK;
+}
+
+void free_model_memory(hdc_model_s* m) {
+  cudaFree(m->Bp);
+  cudaFree(m->Cp);
+  cudaFree(m->bnorm);
+  cudaFree(m->S_part);
+  cudaFree(m->S_grp);
+  cudaFree(m->cnt);
+  cudaFree(m->recheck);
+  cudaFree(m->Xdev);
+  cudaFree(m->ldev);
+  cudaFree(m->sdev);
+}
+
+// Runs the selected path over rows [0, N) of X.
+hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
+                 hdc_path_t path, cudaStream_t st) {
+  m->last_launches = 0;
+  if (N == 0) return HDC_OK;
+  const ModelView mv = m->view();
+  const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC);
+  if (path == HDC_PATH_AUTO) path = HDC_PATH_SMALL;  // fused path: see hdc_fused dispatch
+  if (path == HDC_PATH_FUSED) return fail(HDC_ERR_UNSUPPORTED, "fused path not built yet");
+  const SmallWorkspace ws = m->small_ws();
+  for (int64_t r0 = 0; r0 < N; r0 += kSmallMaxN) {
+    const int n = (int)((N - r0) < kSmallMaxN ? (N - r0) : kSmallMaxN);
+    cudaError_t e = launch_smallbatch(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
+                                      labels ? labels + r0 : nullptr, recheck, st);
+    if (e != cudaSuccess) return cuda_fail(e, "smallbatch launch");
+    ++m->last_launches;
+  }
+  return HDC_OK;
+}
+
+hdc_status_t validate_call(hdc_model_s* m, const float* X, int64_t N, const void* out_required,
+                           const void* out_optional) {
+  if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  if (N < 0) return fail(HDC_ERR_INVALID_VALUE, "N < 0");
+  if (N > 0 && (!X || !out_required)) return fail(HDC_ERR_INVALID_VALUE, "null X or output");
+  if (!aligned(X, 4) || !aligned(out_required, 4) || !aligned(out_optional, 4))
+    return fail(HDC_ERR_MISALIGNED, "pointers must be 4-byte aligned");
+  return HDC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hdc_status_string(hdc_status_t st) {
+  switch (st) {
+    case HDC_OK: return "HDC_OK";
+    case HDC_ERR_INVALID_VALUE: return "HDC_ERR_INVALID_VALUE";
+    case HDC_ERR_MISALIGNED: return "HDC_ERR_MISALIGNED";
+    case HDC_ERR_UNSUPPORTED: return "HDC_ERR_UNSUPPORTED";
+    case HDC_ERR_NO_MEMORY: return "HDC_ERR_NO_MEMORY";
+    case HDC_ERR_CUDA: return "HDC_ERR_CUDA";
+  }
+  return "HDC_ERR_UNKNOWN";
+}
+
+const char* hdc_last_error(void) { return g_last_error.c_str(); }
+
+const char* hdc_version(void) { return "libhdc 0.1 (sm_100a)"; }
+
+hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t D, int64_t K,
+                              hdc_precision_t prec, hdc_model_t* out) {
+  if (!out) return fail(HDC_ERR_INVALID_VALUE, "null out");
+  *out = nullptr;
+  hdc_status_t st = check_dims(F, D, K);
+  if (st != HDC_OK) return st;
+  if (!B || !C) return fail(HDC_ERR_INVALID_VALUE, "null B or C");
+  if (!aligned(B, 4) || !aligned(C, 4)) return fail(HDC_ERR_MISALIGNED, "B, C must be 4-byte aligned");
+  if (prec < HDC_PREC_FP32 || prec > HDC_PREC_FP32_TC) return fail(HDC_ERR_INVALID_VALUE, "bad precision");
+  hdc_model_s* m = new hdc_model_s();
+  m->F = F;
+  m->D = D;
+  m->K = K;
+  m->prec = prec;
+  m->Dp = round_up(D, kDPad);
+  cudaGetDevice(&m->device);
+  const int64_t G = small_num_tiles(D), G1 = small_num_groups(D);
+  cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, bytes)                                           \
+  if (e == cudaSuccess) e = cudaMalloc((void**)&(ptr), (size_t)(bytes));
+  ALLOC(m->Bp, sizeof(float) * F * m->Dp);
+  ALLOC(m->Cp, sizeof(float) * K * m->Dp);
+  ALLOC(m->bnorm, sizeof(float) * m->Dp);
+  ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
+  ALLOC(m->S_grp, sizeof(float) * G1 * kSmallMaxN * K);
+  ALLOC(m->cnt, sizeof(unsigned) * (G1 + 1));
+  ALLOC(m->recheck, sizeof(unsigned long long));
+#undef ALLOC
+  if (e != cudaSuccess) {
+    free_model_memory(m);
+    delete m;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? HDC_ERR_NO_MEMORY : HDC_ERR_CUDA,
+                std::string("model allocation: ") + cudaGetErrorString(e));
+  }
+  cudaStream_t st0 = 0;
+  if (e == cudaSuccess) e = launch_pad_copy(B, F, D, m->Bp, m->Dp, st0);
+  if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
+  if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
+  if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * (G1 + 1));
+  if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    free_model_memory(m);
+    delete m;
+    return cuda_fail(e, "model setup");
+  }
+  *out = m;
+  return HDC_OK;
+}
+
+hdc_status_t hdc_model_destroy(hdc_model_t m) {
+  if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  cudaDeviceSynchronize();
+  free_model_memory(m);
+  delete m;
+  return HDC_OK;
+}
+
+hdc_status_t hdc_model_dims(hdc_model_t m, int64_t* F, int64_t* D, int64_t* K,
+                            hdc_precision_t* prec) {
+  if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  if (F) *F = m->F;
+  if (D) *D = m->D;
+  if (K) *K = m->K;
+  if (prec) *prec = m->prec;
+  return HDC_OK;
+}
+
+hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                                  float* scores, hdc_path_t path, void* stream) {
+  hdc_status_t st = validate_call(m, X, N, labels, scores);
+  if (st != HDC_OK) return st;
+  if (path < HDC_PATH_AUTO || path > HDC_PATH_FUSED) return fail(HDC_ERR_INVALID_VALUE, "bad path");
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
+  return run(m, X, N, labels, scores, path, (cudaStream_t)stream);
+}
+
+hdc_status_t hdc_model_infer(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                             float* scores, void* stream) {
+  return hdc_model_infer_path(m, X, N, labels, scores, HDC_PATH_AUTO, stream);
+}
+
+hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, float* S_partial,
+                                      void* stream) {
+  hdc_status_t st = validate_call(m, X, N, S_partial, nullptr);
+  if (st != HDC_OK) return st;
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
+  return run(m, X, N, nullptr, S_partial, HDC_PATH_SMALL, (cudaStream_t)stream);
+}
+
+hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
+                                  int32_t* labels_host, float* scores_host, void* stream) {
+  hdc_status_t st = validate_call(m, X_host, N, labels_host, scores_host);
+  if (st != HDC_OK) return st;
+  if (N == 0) return HDC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (N > m->Xdev_rows) {
+    cudaStreamSynchronize(s);
+    cudaFree(m->Xdev);
+    cudaFree(m->ldev);
+    cudaFree(m->sdev);
+    m->Xdev = nullptr;
+    m->ldev = nullptr;
+    m->sdev = nullptr;
+    m->Xdev_rows = 0;
+    cudaError_t e = cudaMalloc((void**)&m->Xdev, sizeof(float) * N * m->F);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->ldev, sizeof(int32_t) * N);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->sdev, sizeof(float) * N * m->K);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(HDC_ERR_NO_MEMORY, "staging allocation");
+    }
+    m->Xdev_rows = N;
+  }
+  HDC_CUDA_TRY(cudaMemcpyAsync(m->Xdev, X_host, sizeof(float) * N * m->F, cudaMemcpyHostToDevice, s),
+               "H2D X");
+  st = run(m, m->Xdev, N, m->ldev, scores_host ? m->sdev : nullptr, HDC_PATH_AUTO, s);
+  if (st != HDC_OK) return st;
+  HDC_CUDA_TRY(cudaMemcpyAsync(labels_host, m->ldev, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s),
+               "D2H labels");
+  if (scores_host)
+    HDC_CUDA_TRY(cudaMemcpyAsync(scores_host, m->sdev, sizeof(float) * N * m->K,
+                                 cudaMemcpyDeviceToHost, s),
+                 "D2H scores");
+  return HDC_OK;
+}
+
+hdc_status_t hdc_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, void* stream) {
+  if (N < 0 || K < 1) return fail(HDC_ERR_INVALID_VALUE, "N >= 0, K >= 1 required");
+  if (N > 0 && (!S || !labels)) return fail(HDC_ERR_INVALID_VALUE, "null S or labels");
+  if (!aligned(S, 4) || !aligned(labels, 4)) return fail(HDC_ERR_MISALIGNED, "alignment");
+  cudaError_t e = launch_argmax(S, N, K, labels, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "argmax launch");
+  return HDC_OK;
+}
+
+hdc_status_t hdc_infer(const float* X, const float* B, const float* C, int64_t N, int64_t F,
+                       int64_t D, int64_t K, int32_t* labels, float* scores,
+                       hdc_precision_t prec, void* stream) {
+  hdc_model_t m = nullptr;
+  hdc_status_t st = hdc_model_create(B, C, F, D, K, prec, &m);
+  if (st != HDC_OK) return st;
+  st = hdc_model_infer(m, X, N, labels, scores, stream);
+  hdc_model_destroy(m);
+  return st;
+}
+
+int64_t hdc_model_recheck_count(hdc_model_t m) {
+  if (!m) return -1;
+  unsigned long long v = 0;
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(&v, m->recheck, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)v;
+}
+
+int32_t hdc_model_last_launch_count(hdc_model_t m) { return m ? m->last_launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// k_misc.cu -- K5 row argmax and the model-setup kernels (padding copies, norms).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hdc {
+namespace {
+
+// K5: one warp per row; (value, index) pairs combined so that the lowest index
+// among equal maxima wins (eq. pred_batch; tie rule DESIGN.md R2).
+__global__ void argmax_kernel(const float* __restrict__ S, int64_t N, int64_t K,
+                              int32_t* __restrict__ labels) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= N) return;
+  const float* s = S + row * K;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int64_t k = lane; k < K; k += 32) {
+    const float v = s[k];
+    if (bi == 0x7fffffff || v > bv) { bv = v; bi = (int)k; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) labels[row] = bi;
+}
+
+__global__ void pad_copy_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                float* __restrict__ dst, int64_t dst_cols) {
+  const int64_t total = rows * dst_cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dst_cols, c = i % dst_cols;
+    dst[i] = c < cols ? src[r * cols + c] : 0.f;
+  }
+}
+
+// ||b_d||_2 in float64, rounded UP to fp32 (it only feeds an upper bound).
+__global__ void col_norm_kernel(const float* __restrict__ Bp, int64_t F, int64_t Dp, int64_t D,
+                                float* __restrict__ out) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= Dp) return;
+  double s = 0.0;
+  if (d < D)
+    for (int64_t f = 0; f < F; ++f) {
+      const double b = Bp[f * Dp + d];
+      s = fma(b, b, s);
+    }
+  out[d] = __double2float_ru(__dsqrt_ru(s));
+}
+
+}  // namespace
+
+cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st) {
+  if (N <= 0) return cudaSuccess;
+  const int warps = 8;
+  argmax_kernel<<<(unsigned)((N + warps - 1) / warps), warps * 32, 0, st>>>(S, N, K, labels);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_copy(const float* src, int64_t rows, int64_t cols, float* dst,
+                            int64_t dst_cols, cudaStream_t st) {
+  const int64_t total = rows * dst_cols;
+  if (total <= 0) return cudaSuccess;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  pad_copy_kernel<<<(unsigned)grid, 256, 0, st>>>(src, rows, cols, dst, dst_cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_norms(const float* Bp, int64_t F, int64_t Dp, int64_t D, float* out,
+                             cudaStream_t st) {
+  col_norm_kernel<<<(unsigned)((Dp + 255) / 256), 256, 0, st>>>(Bp, F, Dp, D, out);
+  return cudaGetLastError();
+}
+
+}  // namespace hdc

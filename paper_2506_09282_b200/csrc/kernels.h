@@ -1,0 +1,48 @@
+// kernels.h -- internal launch interface between the C ABI (hdc_api.cu) and the
+// kernels.  Not installed; the public boundary is include/hdc.h.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hdc {
+
+// Model operands in the library's own layout (made by hdc_model_create).
+struct ModelView {
+  int64_t F, D, K;
+  int64_t Dp;            // D padded to a multiple of kDPad (zero columns)
+  const float* Bp;       // F x Dp fp32, zero-padded columns
+  const float* Cp;       // K x Dp fp32, zero-padded columns
+  const float* bnorm;    // Dp: ||b_d||_2 rounded up (0 on padding)
+  float tau_coef;        // sign_bound_coef(F)
+};
+
+constexpr int64_t kDPad = 256;  // D padding granule (covers every kernel's D tile)
+
+// Workspace for the small-batch kernel's cross-CTA reduction.
+struct SmallWorkspace {
+  float* S_part;         // [G][32][K]
+  float* S_grp;          // [G1][32][K]
+  unsigned* cnt1;        // [G1], zero between launches
+  unsigned* cnt2;        // [1],  zero between launches
+  unsigned long long* recheck;  // fp64 re-evaluation counter (diagnostic)
+};
+
+int64_t small_num_tiles(int64_t Dp);     // G
+int64_t small_num_groups(int64_t Dp);    // G1
+
+// K2: rows [0, n) of X (n <= 32), all of D.  Writes S (n x K) to `scores` when
+// non-null and argmax labels to `labels` when non-null.
+cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, const float* X,
+                              int n, float* scores, int32_t* labels, bool recheck,
+                              cudaStream_t st);
+
+// K5: labels[r] = lowest-index argmax of S[r, 0:K).
+cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);
+
+// Model setup helpers.
+cudaError_t launch_pad_copy(const float* src, int64_t rows, int64_t cols, float* dst,
+                            int64_t dst_cols, cudaStream_t st);
+cudaError_t launch_col_norms(const float* Bp, int64_t F, int64_t Dp, int64_t D, float* out,
+                             cudaStream_t st);
+
+}  // namespace hdc

@@ -1,0 +1,175 @@
+"""Thin Python binding of libhdc.so (include/hdc.h) over torch CUDA tensors.
+
+Argument marshalling only: every step of the hot path runs in the library's
+kernels.  There is no fallback: if libhdc.so is missing or a call fails, this
+module raises.
+"""
+import ctypes
+import os
+
+import torch
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhdc.so")
+
+PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp32_tc": 3}
+PATH = {"auto": 0, "small": 1, "fused": 2}
+_STATUS = {0: "HDC_OK", 1: "HDC_ERR_INVALID_VALUE", 2: "HDC_ERR_MISALIGNED",
+           3: "HDC_ERR_UNSUPPORTED", 4: "HDC_ERR_NO_MEMORY", 5: "HDC_ERR_CUDA"}
+
+_lib = None
+
+
+class HDCError(RuntimeError):
+    def __init__(self, status, detail):
+        super().__init__("%s: %s" % (_STATUS.get(status, status), detail))
+        self.status = status
+
+
+def lib():
+    """Load libhdc.so (raises if it has not been built -- no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libhdc.so not found at %s; run __graft_entry__.build()" % LIB_PATH)
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.hdc_infer.argtypes = [P, P, P, I64, I64, I64, I64, P, P, I32, P]
+        L.hdc_model_create.argtypes = [P, P, I64, I64, I64, I32, ctypes.POINTER(P)]
+        L.hdc_model_infer.argtypes = [P, P, I64, P, P, P]
+        L.hdc_model_infer_path.argtypes = [P, P, I64, P, P, I32, P]
+        L.hdc_model_infer_host.argtypes = [P, P, I64, P, P, P]
+        L.hdc_model_partial_scores.argtypes = [P, P, I64, P, P]
+        L.hdc_argmax.argtypes = [P, I64, I64, P, P]
+        L.hdc_model_destroy.argtypes = [P]
+        L.hdc_model_dims.argtypes = [P, P, P, P, P]
+        L.hdc_model_recheck_count.argtypes = [P]
+        L.hdc_model_recheck_count.restype = I64
+        L.hdc_model_last_launch_count.argtypes = [P]
+        L.hdc_model_last_launch_count.restype = ctypes.c_int32
+        L.hdc_status_string.argtypes = [I32]
+        L.hdc_status_string.restype = ctypes.c_char_p
+        L.hdc_last_error.restype = ctypes.c_char_p
+        L.hdc_version.restype = ctypes.c_char_p
+        for name in ("hdc_infer", "hdc_model_create", "hdc_model_infer", "hdc_model_infer_path",
+                     "hdc_model_infer_host", "hdc_model_partial_scores", "hdc_argmax",
+                     "hdc_model_destroy", "hdc_model_dims"):
+            getattr(L, name).restype = I32
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        raise HDCError(status, lib().hdc_last_error().decode())
+
+
+def _stream_ptr(stream, device):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_f32(t, name):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+        raise TypeError("%s must be a CUDA float32 tensor" % name)
+    return t.contiguous()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class Model:
+    """A resident model (hdc_model_create): B (F x D) and C (K x D) on the device."""
+
+    def __init__(self, B, C, prec="fp32"):
+        B = _dev_f32(B, "B")
+        C = _dev_f32(C, "C")
+        if B.dim() != 2 or C.dim() != 2 or B.shape[1] != C.shape[1]:
+            raise ValueError("B must be F x D and C K x D")
+        self.F, self.D = B.shape
+        self.K = C.shape[0]
+        self.prec = prec
+        self.device = B.device
+        self._h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_create(_ptr(B), _ptr(C), self.F, self.D, self.K, PREC[prec],
+                                          ctypes.byref(self._h)))
+
+    def infer(self, X, labels=None, scores=None, path="auto", stream=None, return_scores=False):
+        """Labels (int32 N) and optionally scores (fp32 N x K) for X (N x F)."""
+        X = _dev_f32(X, "X")
+        if X.dim() != 2 or X.shape[1] != self.F:
+            raise ValueError("X must be N x F")
+        N = X.shape[0]
+        if labels is None:
+            labels = torch.empty(N, dtype=torch.int32, device=X.device)
+        if scores is None and return_scores:
+            scores = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_infer_path(self._h, _ptr(X), N, _ptr(labels), _ptr(scores),
+                                              PATH[path], _stream_ptr(stream, X.device)))
+        return labels, scores
+
+    def infer_host(self, X_host, labels_host, scores_host=None, stream=None):
+        """End-to-end call on (pinned) host tensors; asynchronous on `stream`."""
+        if X_host.is_cuda or X_host.dtype != torch.float32 or not X_host.is_contiguous():
+            raise TypeError("X_host must be a contiguous host float32 tensor")
+        N = X_host.shape[0]
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_infer_host(self._h, _ptr(X_host), N, _ptr(labels_host),
+                                              _ptr(scores_host), _stream_ptr(stream, self.device)))
+        return labels_host, scores_host
+
+    def partial_scores(self, X, out=None, stream=None):
+        """Scores over this model's D-slice, no argmax (D-shard piece, Alg. 3)."""
+        X = _dev_f32(X, "X")
+        N = X.shape[0]
+        if out is None:
+            out = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_partial_scores(self._h, _ptr(X), N, _ptr(out),
+                                                  _stream_ptr(stream, X.device)))
+        return out
+
+    def recheck_count(self):
+        return int(lib().hdc_model_recheck_count(self._h))
+
+    def last_launch_count(self):
+        return int(lib().hdc_model_last_launch_count(self._h))
+
+    def close(self):
+        if self._h:
+            _check(lib().hdc_model_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def infer(X, B, C, prec="fp32", return_scores=False, stream=None):
+    """One-shot hdc_infer(X, B, C, N, F, D, K) -> labels (+ scores)."""
+    X, B, C = _dev_f32(X, "X"), _dev_f32(B, "B"), _dev_f32(C, "C")
+    N, F = X.shape
+    D = B.shape[1]
+    K = C.shape[0]
+    labels = torch.empty(N, dtype=torch.int32, device=X.device)
+    scores = torch.empty(N, K, dtype=torch.float32, device=X.device) if return_scores else None
+    with torch.cuda.device(X.device):
+        _check(lib().hdc_infer(_ptr(X), _ptr(B), _ptr(C), N, F, D, K, _ptr(labels), _ptr(scores),
+                               PREC[prec], _stream_ptr(stream, X.device)))
+    return labels, scores
+
+
+def argmax(S, labels=None, stream=None):
+    """Lowest-index row argmax of S (N x K) -> int32 labels (hdc_argmax)."""
+    S = _dev_f32(S, "S")
+    N, K = S.shape
+    if labels is None:
+        labels = torch.empty(N, dtype=torch.int32, device=S.device)
+    with torch.cuda.device(S.device):
+        _check(lib().hdc_argmax(_ptr(S), N, K, _ptr(labels), _stream_ptr(stream, S.device)))
+    return labels
