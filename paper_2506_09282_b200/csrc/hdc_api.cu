@@ -44,9 +44,11 @@ constexpr int kSmallMaxN = 32;
 
 struct hdc_model_s {
   int device = 0;
-  int64_t F = 0, D = 0, K = 0, Dp = 0;
+  int64_t F = 0, D = 0, K = 0, Dp = 0, Fp = 0;
+  int num_sms = 148;
   hdc_precision_t prec = HDC_PREC_FP32;
   float* Bp = nullptr;
+  float* Bt = nullptr;
   float* Cp = nullptr;
   float* bnorm = nullptr;
   // small-batch workspace
@@ -54,6 +56,13 @@ struct hdc_model_s {
   float* S_grp = nullptr;
   unsigned* cnt = nullptr;  // [G1 + 1]
   unsigned long long* recheck = nullptr;
+  // fused-path workspace, grown on demand with N
+  int64_t fw_rows = 0;  // Np capacity
+  int fw_R = 0;
+  float* Xt = nullptr;
+  float* xnorm = nullptr;
+  float* S_part_f = nullptr;
+  unsigned* cnt_f = nullptr;
   // host-buffer (e2e) staging, grown on demand
   float* Xdev = nullptr;
   int64_t Xdev_rows = 0;
@@ -67,7 +76,9 @@ struct hdc_model_s {
     v.D = D;
     v.K = K;
     v.Dp = Dp;
+    v.Fp = Fp;
     v.Bp = Bp;
+    v.Bt = Bt;
     v.Cp = Cp;
     v.bnorm = bnorm;
     v.tau_coef = sign_bound_coef(F);
@@ -96,6 +107,11 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 
 void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Bp);
+  cudaFree(m->Bt);
+  cudaFree(m->Xt);
+  cudaFree(m->xnorm);
+  cudaFree(m->S_part_f);
+  cudaFree(m->cnt_f);
   cudaFree(m->Cp);
   cudaFree(m->bnorm);
   cudaFree(m->S_part);
@@ -107,6 +123,58 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->sdev);
 }
 
+constexpr int64_t kTileM = 128, kTileN = 128;
+
+// Grows the fused workspace to N rows (synchronises only when it grows).
+hdc_status_t ensure_fused_ws(hdc_model_s* m, int64_t N, int R) {
+  const int64_t Tn = (N + kTileM - 1) / kTileM, Np = Tn * kTileM;
+  if (Np <= m->fw_rows && R <= m->fw_R) return HDC_OK;
+  const int64_t rows = Np > m->fw_rows ? Np : m->fw_rows;
+  const int RR = R > m->fw_R ? R : m->fw_R;
+  cudaDeviceSynchronize();
+  cudaFree(m->Xt);
+  cudaFree(m->xnorm);
+  cudaFree(m->S_part_f);
+  cudaFree(m->cnt_f);
+  m->Xt = nullptr; m->xnorm = nullptr; m->S_part_f = nullptr; m->cnt_f = nullptr;
+  m->fw_rows = 0;
+  m->fw_R = 0;
+  cudaError_t e = cudaMalloc((void**)&m->Xt, sizeof(float) * rows * m->Fp);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->xnorm, sizeof(float) * rows);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_f, sizeof(float) * RR * rows * m->K);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_f, sizeof(unsigned) * (rows / kTileM));
+  if (e == cudaSuccess) e = cudaMemset(m->cnt_f, 0, sizeof(unsigned) * (rows / kTileM));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HDC_ERR_NO_MEMORY, "fused workspace allocation");
+  }
+  m->fw_rows = rows;
+  m->fw_R = RR;
+  return HDC_OK;
+}
+
+hdc_status_t run_fused(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
+                       bool recheck, cudaStream_t st) {
+  if (m->prec == HDC_PREC_TF32 || m->prec == HDC_PREC_BF16 || m->prec == HDC_PREC_FP32_TC)
+    return fail(HDC_ERR_UNSUPPORTED, "tensor-core fused path not built yet");
+  const int64_t Tn = (N + kTileM - 1) / kTileM, Td = (m->D + kTileN - 1) / kTileN;
+  const int R = fused_choose_splits(Tn, Td, m->num_sms);
+  hdc_status_t stt = ensure_fused_ws(m, N, R);
+  if (stt != HDC_OK) return stt;
+  FusedWorkspace ws;
+  ws.Xt = m->Xt;
+  ws.xnorm = m->xnorm;
+  ws.S_part = m->S_part_f;
+  ws.cnt = m->cnt_f;
+  ws.recheck = m->recheck;
+  cudaError_t e = launch_prep_x(X, N, m->F, m->Fp, m->Xt, m->xnorm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "prep_x launch");
+  e = launch_fused_ffma(m->view(), ws, X, N, scores, labels, recheck, R, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fused_ffma launch");
+  m->last_launches = 2;
+  return HDC_OK;
+}
+
 // Runs the selected path over rows [0, N) of X.
 hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
                  hdc_path_t path, cudaStream_t st) {
@@ -114,8 +182,8 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   if (N == 0) return HDC_OK;
   const ModelView mv = m->view();
   const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC);
-  if (path == HDC_PATH_AUTO) path = HDC_PATH_SMALL;  // fused path: see hdc_fused dispatch
-  if (path == HDC_PATH_FUSED) return fail(HDC_ERR_UNSUPPORTED, "fused path not built yet");
+  if (path == HDC_PATH_AUTO) path = (N <= kSmallMaxN) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
+  if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
   const SmallWorkspace ws = m->small_ws();
   for (int64_t r0 = 0; r0 < N; r0 += kSmallMaxN) {
     const int n = (int)((N - r0) < kSmallMaxN ? (N - r0) : kSmallMaxN);
@@ -172,12 +240,15 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   m->K = K;
   m->prec = prec;
   m->Dp = round_up(D, kDPad);
+  m->Fp = round_up(F, kFPad);
   cudaGetDevice(&m->device);
+  cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
   const int64_t G = small_num_tiles(D), G1 = small_num_groups(D);
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, bytes)                                           \
   if (e == cudaSuccess) e = cudaMalloc((void**)&(ptr), (size_t)(bytes));
-  ALLOC(m->Bp, sizeof(float) * F * m->Dp);
+  ALLOC(m->Bp, sizeof(float) * m->Fp * m->Dp);
+  ALLOC(m->Bt, sizeof(float) * m->Fp * m->Dp);
   ALLOC(m->Cp, sizeof(float) * K * m->Dp);
   ALLOC(m->bnorm, sizeof(float) * m->Dp);
   ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
@@ -193,7 +264,9 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
                 std::string("model allocation: ") + cudaGetErrorString(e));
   }
   cudaStream_t st0 = 0;
+  if (e == cudaSuccess) e = cudaMemset(m->Bp, 0, sizeof(float) * m->Fp * m->Dp);
   if (e == cudaSuccess) e = launch_pad_copy(B, F, D, m->Bp, m->Dp, st0);
+  if (e == cudaSuccess) e = launch_transpose(m->Bp, m->Fp, m->Dp, m->Bt, st0);
   if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * (G1 + 1));
@@ -247,7 +320,7 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
   if (st != HDC_OK) return st;
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
-  return run(m, X, N, nullptr, S_partial, HDC_PATH_SMALL, (cudaStream_t)stream);
+  return run(m, X, N, nullptr, S_partial, HDC_PATH_AUTO, (cudaStream_t)stream);
 }
 
 hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,

@@ -41,6 +41,21 @@ __global__ void pad_copy_kernel(const float* __restrict__ src, int64_t rows, int
   }
 }
 
+__global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
+                                 float* __restrict__ dst) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    t[k][threadIdx.x] = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[c * rows + r] = t[threadIdx.x][k];
+  }
+}
+
 // ||b_d||_2 in float64, rounded UP to fp32 (it only feeds an upper bound).
 __global__ void col_norm_kernel(const float* __restrict__ Bp, int64_t F, int64_t Dp, int64_t D,
                                 float* __restrict__ out) {
@@ -71,6 +86,13 @@ cudaError_t launch_pad_copy(const float* src, int64_t rows, int64_t cols, float*
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 32) grid = 148 * 32;
   pad_copy_kernel<<<(unsigned)grid, 256, 0, st>>>(src, rows, cols, dst, dst_cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const float* src, int64_t rows, int64_t cols, float* dst,
+                             cudaStream_t st) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst);
   return cudaGetLastError();
 }
 

@@ -9,14 +9,17 @@ namespace hdc {
 // Model operands in the library's own layout (made by hdc_model_create).
 struct ModelView {
   int64_t F, D, K;
+  int64_t Fp;            // F padded to a multiple of kFPad (zero rows)
   int64_t Dp;            // D padded to a multiple of kDPad (zero columns)
-  const float* Bp;       // F x Dp fp32, zero-padded columns
+  const float* Bp;       // Fp x Dp fp32, zero-padded rows and columns
+  const float* Bt;       // Dp x Fp fp32: B transposed (fp64 sign recheck gathers)
   const float* Cp;       // K x Dp fp32, zero-padded columns
   const float* bnorm;    // Dp: ||b_d||_2 rounded up (0 on padding)
   float tau_coef;        // sign_bound_coef(F)
 };
 
 constexpr int64_t kDPad = 256;  // D padding granule (covers every kernel's D tile)
+constexpr int64_t kFPad = 64;   // F padding granule (covers every kernel's K step)
 
 // Workspace for the small-batch kernel's cross-CTA reduction.
 struct SmallWorkspace {
@@ -36,12 +39,31 @@ cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, cons
                               int n, float* scores, int32_t* labels, bool recheck,
                               cudaStream_t st);
 
+// Workspace of the fused large-batch kernels (grown with N).
+struct FusedWorkspace {
+  float* Xt;             // staged X (layout per kernel)
+  float* xnorm;          // [Np] ||x_n||_2
+  float* S_part;         // [R][Np][K]
+  unsigned* cnt;         // [Tn], zero between launches
+  unsigned long long* recheck;
+};
+
+// K1 + K3 (fp32-exact FFMA fused kernel).
+size_t fused_ffma_smem_bytes(int64_t K);
+int fused_choose_splits(int64_t Tn, int64_t Td, int num_sms);
+cudaError_t launch_prep_x(const float* X, int64_t N, int64_t F, int64_t Fp, float* Xt, float* xnorm,
+                          cudaStream_t st);
+cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, const float* X, int64_t N,
+                              float* scores, int32_t* labels, bool recheck, int R, cudaStream_t st);
+
 // K5: labels[r] = lowest-index argmax of S[r, 0:K).
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);
 
 // Model setup helpers.
 cudaError_t launch_pad_copy(const float* src, int64_t rows, int64_t cols, float* dst,
                             int64_t dst_cols, cudaStream_t st);
+cudaError_t launch_transpose(const float* src, int64_t rows, int64_t cols, float* dst,
+                             cudaStream_t st);  // dst[c][r] = src[r][c]
 cudaError_t launch_col_norms(const float* Bp, int64_t F, int64_t Dp, int64_t D, float* out,
                              cudaStream_t st);
 
