@@ -49,6 +49,16 @@ struct hdc_model_s {
   hdc_precision_t prec = HDC_PREC_FP32;
   float* Bp = nullptr;
   float* Bt = nullptr;
+  // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
+  int64_t Dq = 0;            // D rounded up to the tensor-core D tile (80)
+  void* Btc = nullptr;       // [NL][Dq][Fp]
+  double* coltau = nullptr;  // [Dq] (int8 limbs)
+  // tensor-core workspace, grown with N
+  int64_t tw_rows = 0;
+  void* Atc = nullptr;       // [NL][Np][Fp]
+  double* rowtau = nullptr;  // [Np]
+  float* S_part_tc = nullptr;
+  unsigned* cnt_tc = nullptr;
   float* Cp = nullptr;
   float* bnorm = nullptr;
   // small-batch workspace
@@ -106,6 +116,12 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 }
 
 void free_model_memory(hdc_model_s* m) {
+  cudaFree(m->Btc);
+  cudaFree(m->coltau);
+  cudaFree(m->Atc);
+  cudaFree(m->rowtau);
+  cudaFree(m->S_part_tc);
+  cudaFree(m->cnt_tc);
   cudaFree(m->Bp);
   cudaFree(m->Bt);
   cudaFree(m->Xt);
@@ -153,10 +169,89 @@ hdc_status_t ensure_fused_ws(hdc_model_s* m, int64_t N, int R) {
   return HDC_OK;
 }
 
+int tc_mode_of(const hdc_model_s* m) {
+  switch (m->prec) {
+    case HDC_PREC_BF16: return 0;
+    case HDC_PREC_TF32: return 1;
+    case HDC_PREC_FP32_TC: return 2;
+    default: return -1;
+  }
+}
+int tc_limbs(int mode) { return mode == 2 ? 3 : 1; }
+size_t tc_esz(int mode) { return mode == 0 ? 2 : mode == 1 ? 4 : 1; }
+
+bool tc_eligible(const hdc_model_s* m) {
+  const int mode = tc_mode_of(m);
+  if (mode < 0 || m->K > tc_max_k()) return false;
+  if (mode == 2 && m->Fp > tc_max_fp_int8()) return false;
+  return m->Btc != nullptr;
+}
+
+hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
+  const int mode = tc_mode_of(m);
+  const int64_t Np = (N + kTileM - 1) / kTileM * kTileM;
+  if (Np <= m->tw_rows) return HDC_OK;
+  cudaDeviceSynchronize();
+  cudaFree(m->Atc);
+  cudaFree(m->rowtau);
+  cudaFree(m->S_part_tc);
+  cudaFree(m->cnt_tc);
+  m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->cnt_tc = nullptr;
+  m->tw_rows = 0;
+  cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * Np * m->Fp);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(double) * Np);
+  if (e == cudaSuccess)
+    e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * m->num_sms * 2 * kTileM * m->K);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (Np / kTileM));
+  if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (Np / kTileM));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HDC_ERR_NO_MEMORY, "tensor-core workspace allocation");
+  }
+  m->tw_rows = Np;
+  return HDC_OK;
+}
+
+hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
+                          cudaStream_t st) {
+  const int mode = tc_mode_of(m);
+  hdc_status_t stt = ensure_tc_ws(m, N);
+  if (stt != HDC_OK) return stt;
+  const int64_t Np = (N + kTileM - 1) / kTileM * kTileM;
+  cudaError_t e;
+  if (mode == 2)
+    e = launch_tc_limbs(X, N, Np, m->F, m->F, m->Fp, (int8_t*)m->Atc, m->rowtau, tc_tau_const(m->F), st);
+  else
+    e = launch_tc_round(mode, X, N, Np, m->F, m->F, m->Fp, m->Atc, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tensor-core operand staging");
+  TcOperands o;
+  o.F = m->F;
+  o.Fp = m->Fp;
+  o.D = m->D;
+  o.Dp = m->Dp;
+  o.Dq = m->Dq;
+  o.K = m->K;
+  o.N_p = Np;
+  o.A = m->Atc;
+  o.B = m->Btc;
+  o.Cp = m->Cp;
+  o.X = X;
+  o.Bt = m->Bt;
+  o.rowtau = m->rowtau;
+  o.coltau = m->coltau;
+  o.S_part = m->S_part_tc;
+  o.cnt = m->cnt_tc;
+  o.recheck = m->recheck;
+  e = launch_fused_tc(mode, o, N, scores, labels, m->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
+  m->last_launches = 2;
+  return HDC_OK;
+}
+
 hdc_status_t run_fused(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
                        bool recheck, cudaStream_t st) {
-  if (m->prec == HDC_PREC_TF32 || m->prec == HDC_PREC_BF16 || m->prec == HDC_PREC_FP32_TC)
-    return fail(HDC_ERR_UNSUPPORTED, "tensor-core fused path not built yet");
+  if (tc_eligible(m)) return run_fused_tc(m, X, N, labels, scores, st);
+  // fp32 FFMA path (also serves tensor-core precisions with K > 32: more exact, never less)
   const int64_t Tn = (N + kTileM - 1) / kTileM, Td = (m->D + kTileN - 1) / kTileN;
   const int R = fused_choose_splits(Tn, Td, m->num_sms);
   hdc_status_t stt = ensure_fused_ws(m, N, R);
@@ -181,7 +276,8 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   m->last_launches = 0;
   if (N == 0) return HDC_OK;
   const ModelView mv = m->view();
-  const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC);
+  const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC ||
+                        !tc_eligible(m));  // FFMA/small kernels are fp32: keep them sign-exact
   if (path == HDC_PATH_AUTO) path = (N <= kSmallMaxN) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
   if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
   const SmallWorkspace ws = m->small_ws();
@@ -270,6 +366,19 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * (G1 + 1));
+  m->Dq = (D + tc_tile_n() - 1) / tc_tile_n() * tc_tile_n();
+  const int mode = tc_mode_of(m);
+  if (e == cudaSuccess && mode >= 0 && K <= tc_max_k() && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
+    e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);
+    if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(double) * m->Dq);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // Bt must be complete
+    if (e == cudaSuccess) {
+      if (mode == 2)
+        e = launch_tc_limbs(m->Bt, D, m->Dq, F, m->Fp, m->Fp, (int8_t*)m->Btc, m->coltau, 0.0, st0);
+      else
+        e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
+    }
+  }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {

@@ -22,6 +22,7 @@ namespace {
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
 constexpr int HS = BM + 4;           // Hs row stride (floats)
 constexpr int LIST_CAP = 1024;       // flagged-element list per tile
+constexpr int kSaccSmemMaxK = 64;    // larger K keeps the score accumulator in L2
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -104,8 +105,14 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
   float* As = smem;                                  // [STAGES][BK][BM]
   float* Bs = As + STAGES * BK * BM;                 // [STAGES][BK][BN]
   float* Hs = Bs + STAGES * BK * BN;                 // [BN][HS]
-  float* Sacc = Hs + BN * HS;                        // [K][BM]
-  int* list = reinterpret_cast<int*>(Sacc + p.K * BM);  // [LIST_CAP]
+  int* list = reinterpret_cast<int*>(Hs + BN * HS);  // [LIST_CAP]
+  // On-chip N-tile x K score accumulator: shared memory [K][BM] when it fits,
+  // else this CTA's own slice of the partial-score workspace ([BM][K], L2).
+  const int64_t Np = (int64_t)p.Tn * BM;
+  float* part = p.S_part + (int64_t)blockIdx.x * Np * p.K + (int64_t)blockIdx.y * BM * p.K;
+  const bool sacc_smem = p.K <= kSaccSmemMaxK;
+  float* Sacc = sacc_smem ? reinterpret_cast<float*>(list + LIST_CAP) : part;
+  const int64_t sk = sacc_smem ? BM : 1, sm_ = sacc_smem ? 1 : p.K;
   __shared__ int s_nlist;
   __shared__ int s_last;
 
@@ -119,7 +126,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
   const int total = (td1 - td0) * KS;
   const float* Xtile = p.Xt + (int64_t)i * p.Fp * BM;
 
-  for (int e = t; e < p.K * BM; e += THREADS) Sacc[e] = 0.f;
+  for (int e = t; e < p.K * BM; e += THREADS) Sacc[e] = 0.f;  // same extent in both layouts
   if (t == 0) s_nlist = 0;
 
   auto load_stage = [&](int it, int stage) {
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
           float s[8];
           const int kn = min(8, k1 - kc);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) s[kk] = kk < kn ? Sacc[(kc + kk) * BM + m] : 0.f;
+          for (int kk = 0; kk < 8; ++kk) s[kk] = kk < kn ? Sacc[(kc + kk) * sk + m * sm_] : 0.f;
           for (int c4 = 0; c4 < BN / 4; ++c4) {
             const float h0 = Hs[(4 * c4 + 0) * HS + m], h1 = Hs[(4 * c4 + 1) * HS + m];
             const float h2 = Hs[(4 * c4 + 2) * HS + m], h3 = Hs[(4 * c4 + 3) * HS + m];
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
           }
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            if (kk < kn) Sacc[(kc + kk) * BM + m] = s[kk];
+            if (kk < kn) Sacc[(kc + kk) * sk + m * sm_] = s[kk];
         }
       }
       // the next iteration's __syncthreads orders Stage II before the next Hs writes
@@ -264,11 +271,11 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
   __syncthreads();
 
   // ---- partial scores of this D range -> workspace; last CTA of the N-tile reduces.
-  const int64_t Np = (int64_t)p.Tn * BM;
-  float* part = p.S_part + (int64_t)j * Np * p.K + (int64_t)i * BM * p.K;
-  for (int e = t; e < BM * p.K; e += THREADS) {
-    const int m = e / (int)p.K, k = e % (int)p.K;
-    part[e] = Sacc[k * BM + m];
+  if (sacc_smem) {
+    for (int e = t; e < BM * p.K; e += THREADS) {
+      const int m = e / (int)p.K, k = e % (int)p.K;
+      part[e] = Sacc[k * BM + m];
+    }
   }
   __threadfence();
   __syncthreads();
@@ -277,34 +284,41 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
   if (!s_last) return;
   __threadfence();
   const float* base = p.S_part + (int64_t)i * BM * p.K;
-  for (int e = t; e < BM * p.K; e += THREADS) {
-    float s = ld_cg(base + e);
-    for (int jj = 1; jj < p.R; ++jj) s += ld_cg(base + (int64_t)jj * Np * p.K + e);
-    const int m = e / (int)p.K, k = e % (int)p.K;
-    Sacc[k * BM + m] = s;
-    const int64_t row = (int64_t)i * BM + m;
-    if (p.scores && row < p.N) p.scores[row * p.K + k] = s;
+  float* Sfin = Hs;  // [128][BM] scratch: classes handled in chunks of 128
+  int best = 0;
+  float bestv = 0.f;
+  for (int kc = 0; kc < (int)p.K; kc += 128) {       // Hs holds 128 classes x BM rows
+    const int kn = min(128, (int)p.K - kc);
+    for (int e = t; e < BM * kn; e += THREADS) {
+      const int m = e / kn, k = kc + e % kn;
+      const int64_t off = (int64_t)m * p.K + k;
+      float s = ld_cg(base + off);
+      for (int jj = 1; jj < p.R; ++jj) s += ld_cg(base + (int64_t)jj * Np * p.K + off);
+      Sfin[(k - kc) * BM + m] = s;
+      const int64_t row = (int64_t)i * BM + m;
+      if (p.scores && row < p.N) p.scores[row * p.K + k] = s;
+    }
+    __syncthreads();
+    if (t < BM) {
+      for (int k = 0; k < kn; ++k) {
+        const float v = Sfin[k * BM + t];
+        if ((kc == 0 && k == 0) || v > bestv) { bestv = v; best = kc + k; }
+      }
+    }
+    __syncthreads();
   }
   if (t == 0) p.cnt[i] = 0u;
-  __syncthreads();
   if (p.labels && t < BM) {
     const int64_t row = (int64_t)i * BM + t;
-    if (row < p.N) {
-      int best = 0;
-      float bv = Sacc[t];
-      for (int k = 1; k < (int)p.K; ++k) {
-        const float v = Sacc[k * BM + t];
-        if (v > bv) { bv = v; best = k; }
-      }
-      p.labels[row] = best;
-    }
+    if (row < p.N) p.labels[row] = best;
   }
 }
 
 }  // namespace
 
 size_t fused_ffma_smem_bytes(int64_t K) {
-  return sizeof(float) * ((size_t)STAGES * BK * (BM + BN) + (size_t)BN * HS + (size_t)K * BM) +
+  return sizeof(float) * ((size_t)STAGES * BK * (BM + BN) + (size_t)BN * HS +
+                          (K <= kSaccSmemMaxK ? (size_t)K * BM : 0)) +
          sizeof(int) * LIST_CAP;
 }
 

@@ -1,0 +1,599 @@
+// k_fused_tc.cu -- K4: fused large-batch HDC inference on the 5th-gen tensor
+// cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Alg. 1 per (N-tile of 128 rows) x (D-tile of 80 columns):
+//   Stage I   V_tile = X_tile B_tile on tcgen05.mma, accumulators in TMEM;
+//   act       HardSign in registers after tcgen05.ld;
+//   Stage II  S_local[n, :] += H_tile[n, :] C_tile^T with FFMA in the epilogue
+//             warps, the S accumulator kept in registers for the CTA's run of
+//             D-tiles (ScalableHD-L row ownership, Alg. 4).
+// H never leaves the SM.
+//
+// Precision modes (hdc_precision_t):
+//   BF16  X, B rounded to bf16 (RN); kind::f16, fp32 accumulate.
+//   TF32  X, B rounded to tf32 (RNA); kind::tf32, fp32 accumulate.
+//   INT8x3 ("FP32_TC", sign-exact): per-row/column scaled 21-bit integer
+//         images of X and B split into three balanced base-128 int8 limbs;
+//         the six limb products with i + j <= 2 run as kind::i8 MMAs with EXACT
+//         int32 accumulation into three TMEM accumulators, combined in int64.
+//         The rigorous error bound of that integer image flags
+//         the few |I| <= tau, which are re-evaluated in float64 -> every
+//         HardSign decision equals that of the exact product X B.
+//
+// Warp roles (384 threads, one CTA per SM, persistent over a contiguous range
+// of the n-major tile sequence): warp 0 TMA producer, warp 1 MMA issuer (and
+// TMEM owner), warps 4..11 epilogue (warp w reads TMEM lanes 32*(w%4).. and
+// the column half (w-4)/4).  smem ring: 4 stages x {A limbs, B limbs} with
+// SWIZZLE_64B K-major tiles; TMEM: 2 accumulator buffers x 256 columns.
+// Partial scores of N-tiles shared between CTAs are summed in CTA order by the
+// last-arriving CTA, which takes the lowest-index argmax: deterministic.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace hdc {
+namespace {
+
+using namespace ptx;
+
+constexpr int BM = 128;              // rows per tile (MMA M)
+constexpr int BN = 80;               // D columns per tile (MMA N); 10000 = 125 x 80
+constexpr int KBYTES = 64;           // K bytes per stage (SWIZZLE_64B atom row)
+constexpr int STAGES = 4;
+constexpr int THREADS = 384;
+constexpr int EPI_WARP0 = 4;
+constexpr int NUM_EPI = 8;
+constexpr int HALF = BN / 2;         // columns per epilogue warp
+constexpr int ACC_BUF_COLS = 256;    // TMEM columns per accumulator buffer
+constexpr int MAX_LIMBS = 3;
+constexpr int A_LIMB_BYTES = BM * KBYTES;            // 8192
+constexpr int B_LIMB_BYTES = BN * KBYTES;            // 5120
+constexpr int A_STAGE_BYTES = MAX_LIMBS * A_LIMB_BYTES;
+constexpr int B_STAGE_BYTES = MAX_LIMBS * B_LIMB_BYTES;
+constexpr int KT_MAX = 32;           // classes handled by this kernel (registers)
+constexpr int C_SLOT_BYTES = KT_MAX * BN * 4;        // fp32 C tile [K][80]
+constexpr int RED_BYTES = BM * KT_MAX * 4;
+
+struct SmemLayout {
+  static constexpr int a = 0;
+  static constexpr int b = a + STAGES * A_STAGE_BYTES;
+  static constexpr int c = b + STAGES * B_STAGE_BYTES;
+  static constexpr int red = c + 2 * C_SLOT_BYTES;
+  static constexpr int bars = red + RED_BYTES;
+  static constexpr int total = bars + 256;
+};
+
+struct TcParams {
+  int64_t N, F, Fp, D, Dp, Dq, K, Np;
+  int Tn, Td, G;
+  int64_t T;
+  const float* X;          // caller's X (fp64 recheck)
+  const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
+  const double* rowtau;    // int8 mode: per-row part of tau (integer units)
+  const double* coltau;    // int8 mode: per-column part of tau
+  float* S_part;           // [G][2][BM][K]
+  unsigned* cnt;           // [Tn]
+  unsigned long long* recheck_count;
+  float* scores;
+  int32_t* labels;
+};
+
+__device__ __forceinline__ int64_t range_begin(int c, int64_t T, int G) { return (int64_t)c * T / G; }
+__device__ __forceinline__ int owner_of(int64_t t, int64_t T, int G) {
+  int c = (int)((t * G) / T);
+  while (c + 1 < G && range_begin(c + 1, T, G) <= t) ++c;
+  while (c > 0 && range_begin(c, T, G) > t) --c;
+  return c;
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// float64 re-evaluation of V[row, d] (fixed lane order, warp-cooperative).
+__device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, int64_t d, int lane) {
+  const float* xr = p.X + row * p.F;
+  const float* br = p.Bt + d * p.Fp;
+  double s = 0.0;
+  for (int64_t f = lane; f < p.F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
+  s = warp_sum_xor(s);
+  return s >= 0.0 ? 1.f : -1.f;
+}
+
+template <int MODE, int KT>  // MODE: 0 bf16, 1 tf32, 2 int8x3
+__global__ void __launch_bounds__(THREADS, 1)
+fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+  constexpr int NL = (MODE == 2) ? 3 : 1;
+  constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;   // element bytes
+  constexpr int KE = KBYTES / ESZ;                            // K elements per stage
+  constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
+  constexpr uint32_t STAGE_TX = NL * (A_LIMB_BYTES + B_LIMB_BYTES);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the swizzled operand tiles
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem + SmemLayout::a;
+  uint8_t* sB = smem + SmemLayout::b;
+  float* sC = reinterpret_cast<float*>(smem + SmemLayout::c);
+  float* sRed = reinterpret_cast<float*>(smem + SmemLayout::red);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* cfull = tempty + 2;          // [2]
+  uint64_t* cempty = cfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int64_t t0 = range_begin(c, p.T, p.G), t1 = range_begin(c + 1, p.T, p.G);
+  const int KB = (int)(p.Fp / KE);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, NUM_EPI);
+      mbar_init(cfull + b, 1);
+      mbar_init(cempty + b, NUM_EPI);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int cs = 0;
+      uint32_t cphase = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
+        mbar_wait(cempty + cs, cphase ^ 1);
+        mbar_arrive_expect_tx(cfull + cs, (uint32_t)(p.K * BN * 4));
+        tma_load_2d(sC + cs * (C_SLOT_BYTES / 4), &tmC, cfull + cs, di * BN, 0);
+        cs ^= 1;
+        if (cs == 0) cphase ^= 1;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_arrive_expect_tx(full + stage, STAGE_TX);
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            tma_load_2d(sA + stage * A_STAGE_BYTES + l * A_LIMB_BYTES, &tmA, full + stage, kb * KE,
+                        (int)(l * p.Np + (int64_t)ni * BM));
+            tma_load_2d(sB + stage * B_STAGE_BYTES + l * B_LIMB_BYTES, &tmB, full + stage, kb * KE,
+                        (int)(l * p.Dq + (int64_t)di * BN));
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int buf = 0;
+      uint32_t bphase = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        mbar_wait(tempty + buf, bphase ^ 1);
+        tc_fence_after();
+        const uint32_t acc0 = tmem_base + buf * ACC_BUF_COLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < KBYTES / 32; ++ks) {
+            const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
+            if constexpr (MODE == 2) {
+              uint64_t a[3], b[3];
+#pragma unroll
+              for (int l = 0; l < 3; ++l) {
+                a[l] = smem_desc_sw64(a_base + l * A_LIMB_BYTES + ks * 32);
+                b[l] = smem_desc_sw64(b_base + l * B_LIMB_BYTES + ks * 32);
+              }
+              // A0 += x0 b0 ; A1 += x0 b1 + x1 b0 ; A2 += x0 b2 + x1 b1 + x2 b0
+              tc_mma<2>(acc0 + 0 * BN, a[0], b[0], IDESC, first);
+              tc_mma<2>(acc0 + 1 * BN, a[0], b[1], IDESC, first);
+              tc_mma<2>(acc0 + 1 * BN, a[1], b[0], IDESC, 1u);
+              tc_mma<2>(acc0 + 2 * BN, a[0], b[2], IDESC, first);
+              tc_mma<2>(acc0 + 2 * BN, a[1], b[1], IDESC, 1u);
+              tc_mma<2>(acc0 + 2 * BN, a[2], b[0], IDESC, 1u);
+            } else {
+              tc_mma<MODE>(acc0, smem_desc_sw64(a_base + ks * 32), smem_desc_sw64(b_base + ks * 32),
+                           IDESC, first);
+            }
+          }
+          tc_commit(empty + stage);          // frees the smem stage when these MMAs finish
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull + buf);              // accumulators of this tile are ready
+        buf ^= 1;
+        if (buf == 0) bphase ^= 1;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================================================== epilogue
+    const int ew = warp - EPI_WARP0;
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int half = ew >> 2;               // column half of the 80-wide tile
+    const int m = q * 32 + lane;            // row within the N-tile
+    const int K = (int)p.K;
+    float S[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) S[k] = 0.f;
+    int buf = 0;
+    uint32_t bphase = 0;
+    int cs = 0;
+    uint32_t cphase = 0;
+    unsigned long long nrecheck = 0;
+    const int first_ni = (int)(t0 / p.Td);
+    for (int64_t t = t0; t < t1; ++t) {
+      const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
+      const int64_t row = (int64_t)ni * BM + m;
+      const bool row_ok = row < p.N;
+      double rtau = 0.0;
+      if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : 0.0;
+      mbar_wait(tfull + buf, bphase);
+      tc_fence_after();
+      mbar_wait(cfull + cs, cphase);
+      const float* cslot = sC + cs * (C_SLOT_BYTES / 4);
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * ACC_BUF_COLS + half * HALF;
+#pragma unroll 1
+      for (int ch = 0; ch < HALF / 8; ++ch) {
+        const int col0 = half * HALF + ch * 8;      // column within the tile
+        float h[8];
+        if constexpr (MODE == 2) {
+          uint32_t r0[8], r1[8], r2[8];
+          tmem_ld8(tbase + ch * 8, r0);
+          tmem_ld8(tbase + BN + ch * 8, r1);
+          tmem_ld8(tbase + 2 * BN + ch * 8, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
+                              (int64_t)(int32_t)r2[j];
+            h[j] = I >= 0 ? 1.f : -1.f;
+            const int64_t d = (int64_t)di * BN + col0 + j;
+            const bool flag = row_ok && d < p.D &&
+                              fabs((double)I) <= rtau + __ldg(p.coltau + d);
+            unsigned mask = __ballot_sync(0xffffffffu, flag);
+            while (mask) {
+              const int src = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const int64_t srow = (int64_t)ni * BM + q * 32 + src;
+              const float hv = recheck_warp(p, srow, d, lane);
+              if (lane == src) h[j] = hv;
+              ++nrecheck;
+            }
+          }
+        } else {
+          uint32_t r0[8];
+          tmem_ld8(tbase + ch * 8, r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = hardsign(__uint_as_float(r0[j]));
+        }
+        // Stage II: S[k] += h[c] * C[k, d0 + c]  (padded columns have C = 0)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (k < K) S[k] = fmaf(h[j], cslot[k * BN + col0 + j], S[k]);
+        }
+      }
+      // release the TMEM buffer and the C slot
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(tempty + buf);
+        mbar_arrive(cempty + cs);
+      }
+      buf ^= 1;
+      if (buf == 0) bphase ^= 1;
+      cs ^= 1;
+      if (cs == 0) cphase ^= 1;
+
+      // ---- end of this CTA's run of D-tiles for N-tile ni?
+      const bool seg_end = (t + 1 == t1) || ((t + 1) / p.Td != ni);
+      if (!seg_end) continue;
+      // combine the two column halves (fixed order: half 0 + half 1)
+      if (half == 1) {
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < K) sRed[k * BM + m] = S[k];
+      }
+      named_bar(1, NUM_EPI * 32);
+      const int c_first = owner_of((int64_t)ni * p.Td, p.T, p.G);
+      const int c_last = owner_of((int64_t)(ni + 1) * p.Td - 1, p.T, p.G);
+      const bool sole = (c_first == c_last);
+      if (half == 0) {
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < K) S[k] = S[k] + sRed[k * BM + m];
+        if (!sole) {
+          const int slot = (ni == first_ni) ? 0 : 1;
+          float* part = p.S_part + (((int64_t)c * 2 + slot) * BM + m) * p.K;
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (k < K) part[k] = S[k];
+          __threadfence();
+        }
+      }
+      named_bar(1, NUM_EPI * 32);
+      if (!sole && threadIdx.x == EPI_WARP0 * 32) {
+        const unsigned prev = atomicAdd(p.cnt + ni, 1u);
+        *s_flag = (prev == (unsigned)(c_last - c_first)) ? 1 : 0;
+        if (*s_flag) p.cnt[ni] = 0u;
+      }
+      named_bar(1, NUM_EPI * 32);
+      const bool finalize = sole || (*s_flag != 0);
+      if (finalize && half == 0) {
+        if (!sole) {
+          __threadfence();
+#pragma unroll
+          for (int k = 0; k < KT; ++k) S[k] = 0.f;
+          for (int cc = c_first; cc <= c_last; ++cc) {
+            const int slot = ((int)(range_begin(cc, p.T, p.G) / p.Td) == ni) ? 0 : 1;
+            const float* part = p.S_part + (((int64_t)cc * 2 + slot) * BM + m) * p.K;
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if (k < K) S[k] = (cc == c_first) ? ld_cg(part + k) : S[k] + ld_cg(part + k);
+          }
+        }
+        if (row_ok) {
+          int best = 0;
+          float bv = S[0];
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            if (k < K) {
+              if (p.scores) p.scores[row * p.K + k] = S[k];
+              if (k > 0 && S[k] > bv) {
+                bv = S[k];
+                best = k;
+              }
+            }
+          }
+          if (p.labels) p.labels[row] = best;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KT; ++k) S[k] = 0.f;
+      named_bar(1, NUM_EPI * 32);   // sRed / s_flag reuse
+    }
+    if (MODE == 2) {
+      // one atomic per warp (lane 0 holds the warp's count: all lanes counted the same items)
+      if (lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
+    }
+  }
+  __syncwarp();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- operand prep
+// Balanced base-128 digits of the 21-bit integer image U = rint(x * c).
+__device__ __forceinline__ void limbs_of(float x, float c, int& d0, int& d1, int& d2, int& U) {
+  int u = __float2int_rn(x * c);
+  u = max(-2080768, min(2080768, u));
+  d2 = ((u + 64) & 127) - 64;
+  const int u1 = (u - d2) >> 7;
+  d1 = ((u1 + 64) & 127) - 64;
+  d0 = (u1 - d1) >> 7;
+  U = u;
+}
+
+__device__ __forceinline__ float scale_for(float amax) {
+  if (!(amax > 0.f)) return 1.f;
+  double c = 2080768.0 / (double)amax;
+  if (c > 1e37) c = 1e37;
+  return (float)c * (1.f - 9.5367431640625e-07f);  // (1 - 2^-20): keeps |x c| < 127*2^14
+}
+
+// One warp per row of a row-major [rows][F] fp32 matrix (X rows, or B^T rows):
+// int8 limbs into out[l][rows_p][Fp] and the per-row tau term.
+__global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
+                                 int64_t F, int64_t ld_src, int64_t Fp, int8_t* __restrict__ out,
+                                 double* __restrict__ tau_part, double tau_const) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows_p) return;
+  const bool valid = r < rows;
+  float amax = 0.f;
+  if (valid)
+    for (int64_t f = lane; f < F; f += 32) amax = fmaxf(amax, fabsf(src[r * ld_src + f]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float c = scale_for(amax);
+  long long l1 = 0;
+  for (int64_t f = lane; f < Fp; f += 32) {
+    const float x = (valid && f < F) ? src[r * ld_src + f] : 0.f;
+    int d0, d1, d2, U;
+    limbs_of(x, c, d0, d1, d2, U);
+    out[(0 * rows_p + r) * Fp + f] = (int8_t)d0;
+    out[(1 * rows_p + r) * Fp + f] = (int8_t)d1;
+    out[(2 * rows_p + r) * Fp + f] = (int8_t)d2;
+    l1 += U < 0 ? -U : U;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  // |c_x c_b x.b - U_x.U_b| <= 0.625 (L1(U_x) + L1(U_b)) + 0.3907 F and the dropped limb
+  // products (i + j >= 3) add <= F (2^20 + 2^12).  The kernel compares in
+  // units of 2^14 (I = A0 2^14 + A1 2^7 + A2 = U_x.U_b / 2^14 without the dropped terms).
+  if (lane == 0 && tau_part)
+    tau_part[r] = valid ? (0.625 * (double)l1 * (1.0 + 1e-12) + tau_const) * (1.0 / 16384.0) : 0.0;
+}
+
+// Rounded copies for the bf16 / tf32 modes: out[r][f] (rows_p x Fp, zero padded).
+template <int MODE>
+__global__ void round_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
+                                  int64_t F, int64_t ld_src, int64_t Fp, void* __restrict__ out) {
+  const int64_t total = rows_p * Fp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / Fp, f = i % Fp;
+    const float x = (r < rows && f < F) ? src[r * ld_src + f] : 0.f;
+    if constexpr (MODE == 0) {
+      reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(x);
+    } else {
+      uint32_t y;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+      reinterpret_cast<uint32_t*>(out)[i] = y;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* base, uint64_t inner,
+                 uint64_t outer, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * (uint64_t)esz};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE, int KT>
+cudaError_t launch_mode_kt(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
+                           const TcParams& p, cudaStream_t st) {
+  const size_t sm = SmemLayout::total + 1024;
+  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE, KT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  fused_tc_kernel<MODE, KT><<<p.G, THREADS, sm, st>>>(a, b, cm, p);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
+                        const TcParams& p, cudaStream_t st) {
+  if (p.K <= 8) return launch_mode_kt<MODE, 8>(a, b, cm, p, st);
+  if (p.K <= 16) return launch_mode_kt<MODE, 16>(a, b, cm, p, st);
+  return launch_mode_kt<MODE, 32>(a, b, cm, p, st);
+}
+
+}  // namespace
+
+int tc_tile_n() { return BN; }
+int tc_max_k() { return KT_MAX; }
+int64_t tc_max_fp_int8() { return 100000; }
+
+double tc_tau_const(int64_t F) { return (double)F * (0.390625 + 1048576.0 + 4096.0) * (1.0 + 1e-12) + 1.0; }
+
+cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
+                            int64_t Fp, int8_t* out, double* tau_part, double tau_const,
+                            cudaStream_t st) {
+  const int warps = 8;
+  limb_rows_kernel<<<(unsigned)((rows_p + warps - 1) / warps), warps * 32, 0, st>>>(
+      src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t rows_p, int64_t F,
+                            int64_t ld_src, int64_t Fp, void* out, cudaStream_t st) {
+  const int64_t total = rows_p * Fp;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  if (mode == 0)
+    round_rows_kernel<0><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out);
+  else
+    round_rows_kernel<1><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
+                            int num_sms, cudaStream_t st) {
+  const int64_t Tn = (o.N_p) / BM;
+  const int64_t Td = (o.D + BN - 1) / BN;
+  TcParams p;
+  p.N = N;
+  p.F = o.F;
+  p.Fp = o.Fp;
+  p.D = o.D;
+  p.Dp = o.Dp;
+  p.Dq = o.Dq;
+  p.K = o.K;
+  p.Np = o.N_p;
+  p.Tn = (int)Tn;
+  p.Td = (int)Td;
+  p.T = Tn * Td;
+  p.G = (int)(p.T < num_sms ? p.T : num_sms);
+  p.X = o.X;
+  p.Bt = o.Bt;
+  p.rowtau = o.rowtau;
+  p.coltau = o.coltau;
+  p.S_part = o.S_part;
+  p.cnt = o.cnt;
+  p.recheck_count = o.recheck;
+  p.scores = scores;
+  p.labels = labels;
+  const int nl = (mode == 2) ? 3 : 1;
+  const int esz = (mode == 0) ? 2 : (mode == 1) ? 4 : 1;
+  const CUtensorMapDataType dt = (mode == 0)   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                               : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  CUtensorMap ma, mb, mc;
+  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, KBYTES / esz, BM,
+                   CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, KBYTES / esz, BN,
+                   CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map_2d(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, o.Cp, (uint64_t)o.Dp, (uint64_t)o.K, BN,
+                   (uint32_t)o.K, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  if (mode == 0) return launch_mode<0>(ma, mb, mc, p, st);
+  if (mode == 1) return launch_mode<1>(ma, mb, mc, p, st);
+  return launch_mode<2>(ma, mb, mc, p, st);
+}
+
+}  // namespace hdc

