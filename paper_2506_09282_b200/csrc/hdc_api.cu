@@ -52,11 +52,12 @@ struct hdc_model_s {
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
   int64_t Dq = 0;            // D rounded up to the tensor-core D tile (80)
   void* Btc = nullptr;       // [NL][Dq][Fp]
-  double* coltau = nullptr;  // [Dq] (int8 limbs)
+  int64_t* coltau = nullptr; // [Dq] (int8 limbs)
+  void* Cil = nullptr;       // [Td][2][Kp*80] bf16 hi/lo C tiles for the Stage II MMA
   // tensor-core workspace, grown with N
   int64_t tw_rows = 0;
   void* Atc = nullptr;       // [NL][Np][Fp]
-  double* rowtau = nullptr;  // [Np]
+  int64_t* rowtau = nullptr; // [Np]
   float* S_part_tc = nullptr;
   unsigned* cnt_tc = nullptr;
   float* Cp = nullptr;
@@ -118,6 +119,7 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Btc);
   cudaFree(m->coltau);
+  cudaFree(m->Cil);
   cudaFree(m->Atc);
   cudaFree(m->rowtau);
   cudaFree(m->S_part_tc);
@@ -182,7 +184,7 @@ size_t tc_esz(int mode) { return mode == 0 ? 2 : mode == 1 ? 4 : 1; }
 
 bool tc_eligible(const hdc_model_s* m) {
   const int mode = tc_mode_of(m);
-  if (mode < 0 || m->K > tc_max_k()) return false;
+  if (mode < 0 || m->K > tc_max_k(mode)) return false;
   if (mode == 2 && m->Fp > tc_max_fp_int8()) return false;
   return m->Btc != nullptr;
 }
@@ -199,7 +201,7 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->cnt_tc = nullptr;
   m->tw_rows = 0;
   cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * Np * m->Fp);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(double) * Np);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(int64_t) * Np);
   if (e == cudaSuccess)
     e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * m->num_sms * 2 * kTileM * m->K);
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (Np / kTileM));
@@ -234,7 +236,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.N_p = Np;
   o.A = m->Atc;
   o.B = m->Btc;
-  o.Cp = m->Cp;
+  o.Cil = m->Cil;
   o.X = X;
   o.Bt = m->Bt;
   o.rowtau = m->rowtau;
@@ -368,16 +370,18 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * (G1 + 1));
   m->Dq = (D + tc_tile_n() - 1) / tc_tile_n() * tc_tile_n();
   const int mode = tc_mode_of(m);
-  if (e == cudaSuccess && mode >= 0 && K <= tc_max_k() && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
+  if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
     e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);
-    if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(double) * m->Dq);
+    if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(int64_t) * m->Dq);
+    if (e == cudaSuccess) e = cudaMalloc(&m->Cil, (size_t)2 * 2 * tc_kp(K) * m->Dq);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // Bt must be complete
     if (e == cudaSuccess) {
       if (mode == 2)
-        e = launch_tc_limbs(m->Bt, D, m->Dq, F, m->Fp, m->Fp, (int8_t*)m->Btc, m->coltau, 0.0, st0);
+        e = launch_tc_limbs(m->Bt, D, m->Dq, F, m->Fp, m->Fp, (int8_t*)m->Btc, m->coltau, 0, st0);
       else
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
+    if (e == cudaSuccess) e = launch_tc_c_interleave(m->Cp, K, tc_kp(K), D, m->Dp, m->Cil, st0);
   }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

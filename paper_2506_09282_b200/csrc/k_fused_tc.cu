@@ -2,31 +2,35 @@
 // cores (tcgen05 + TMEM + TMA), sm_100a.
 //
 // Alg. 1 per (N-tile of 128 rows) x (D-tile of 80 columns):
-//   Stage I   V_tile = X_tile B_tile on tcgen05.mma, accumulators in TMEM;
-//   act       HardSign in registers after tcgen05.ld;
-//   Stage II  S_local[n, :] += H_tile[n, :] C_tile^T with FFMA in the epilogue
-//             warps, the S accumulator kept in registers for the CTA's run of
-//             D-tiles (ScalableHD-L row ownership, Alg. 4).
+//   Stage I   V_tile = X_tile B_tile: tcgen05.mma, accumulators in TMEM
+//             (eq. batch_encode);
+//   act       HardSign in the epilogue warps after tcgen05.ld, written
+//             as exact bf16 +-1 into a shared-memory H tile;
+//   Stage II  S[n, :] += H_tile C_tile^T as a second tcgen05.mma (bf16, C split
+//             into hi + lo bf16 parts) into a TMEM accumulator that lives for the
+//             CTA's whole run of D-tiles of one N-tile (eq. batch_sim P:180-183;
+//             ScalableHD-L row ownership, Alg. 4).
 // H never leaves the SM.
 //
 // Precision modes (hdc_precision_t):
 //   BF16  X, B rounded to bf16 (RN); kind::f16, fp32 accumulate.
 //   TF32  X, B rounded to tf32 (RNA); kind::tf32, fp32 accumulate.
-//   INT8x3 ("FP32_TC", sign-exact): per-row/column scaled 21-bit integer
-//         images of X and B split into three balanced base-128 int8 limbs;
-//         the six limb products with i + j <= 2 run as kind::i8 MMAs with EXACT
-//         int32 accumulation into three TMEM accumulators, combined in int64.
-//         The rigorous error bound of that integer image flags
-//         the few |I| <= tau, which are re-evaluated in float64 -> every
-//         HardSign decision equals that of the exact product X B.
+//   INT8x3 (HDC_PREC_FP32_TC, sign-exact): per-row/column scaled 21-bit integer
+//         images of X and B split into three balanced base-128 int8 limbs; the
+//         six limb products with i + j <= 2 run as kind::i8 MMAs with EXACT int32
+//         accumulation into three TMEM accumulators, combined in int64.  The
+//         rigorous bound of that integer image flags the few
+//         |I| <= tau, re-evaluated in float64 -> every HardSign decision equals
+//         that of the exact product X B.
 //
 // Warp roles (384 threads, one CTA per SM, persistent over a contiguous range
 // of the n-major tile sequence): warp 0 TMA producer, warp 1 MMA issuer (and
 // TMEM owner), warps 4..11 epilogue (warp w reads TMEM lanes 32*(w%4).. and
-// the column half (w-4)/4).  smem ring: 4 stages x {A limbs, B limbs} with
-// SWIZZLE_64B K-major tiles; TMEM: 2 accumulator buffers x 256 columns.
-// Partial scores of N-tiles shared between CTAs are summed in CTA order by the
-// last-arriving CTA, which takes the lowest-index argmax: deterministic.
+// column half (w-4)/4).  smem: 4-stage ring of SWIZZLE_64B K-major operand
+// tiles, 2 H tiles, 2 C tiles (interleaved K-major bf16 hi/lo); TMEM: two
+// Stage I accumulator buffers + the Stage II accumulator.  Partial scores of
+// N-tiles split between CTAs are summed in CTA order by the last-arriving CTA,
+// which takes the lowest-index argmax: bit-deterministic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -40,40 +44,55 @@ namespace {
 using namespace ptx;
 
 constexpr int BM = 128;              // rows per tile (MMA M)
-constexpr int BN = 80;               // D columns per tile (MMA N); 10000 = 125 x 80
+constexpr int BN = 80;               // D columns per tile; 10000 = 125 x 80
 constexpr int KBYTES = 64;           // K bytes per stage (SWIZZLE_64B atom row)
 constexpr int STAGES = 4;
 constexpr int THREADS = 384;
 constexpr int EPI_WARP0 = 4;
 constexpr int NUM_EPI = 8;
 constexpr int HALF = BN / 2;         // columns per epilogue warp
-constexpr int ACC_BUF_COLS = 256;    // TMEM columns per accumulator buffer
 constexpr int MAX_LIMBS = 3;
 constexpr int A_LIMB_BYTES = BM * KBYTES;            // 8192
 constexpr int B_LIMB_BYTES = BN * KBYTES;            // 5120
 constexpr int A_STAGE_BYTES = MAX_LIMBS * A_LIMB_BYTES;
 constexpr int B_STAGE_BYTES = MAX_LIMBS * B_LIMB_BYTES;
-constexpr int KT_MAX = 32;           // classes handled by this kernel (registers)
-constexpr int C_SLOT_BYTES = KT_MAX * BN * 4;        // fp32 C tile [K][80]
-constexpr int RED_BYTES = BM * KT_MAX * 4;
+constexpr int H_BYTES = BM * BN * 2;                 // bf16 H tile (interleaved K-major)
+constexpr int CORE_LBO = 128;                        // K-adjacent 8x16B core matrices
+constexpr int CORE_SBO = (BN / 8) * 128;             // 8-row groups (10 core matrices)
+constexpr int KP_MAX_I8 = 32;                        // Stage II N (classes) limits
+constexpr int KP_MAX_16 = 128;
+constexpr int C_SLOT_MAX = 2 * KP_MAX_16 * BN * 2;   // bf16 hi + lo, [Kp][80] each
 
-struct SmemLayout {
-  static constexpr int a = 0;
-  static constexpr int b = a + STAGES * A_STAGE_BYTES;
-  static constexpr int c = b + STAGES * B_STAGE_BYTES;
-  static constexpr int red = c + 2 * C_SLOT_BYTES;
-  static constexpr int bars = red + RED_BYTES;
-  static constexpr int total = bars + 256;
+template <int MODE>
+struct Cfg {
+  static constexpr int NL = (MODE == 2) ? 3 : 1;
+  static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
+  static constexpr int KE = KBYTES / ESZ;                      // K elements per stage
+  static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : 128;  // TMEM cols per Stage I buffer
+  static constexpr int D2_COL = (MODE == 2) ? 480 : 256;          // Stage II accumulator
+  static constexpr int KP_MAX = (MODE == 2) ? KP_MAX_I8 : KP_MAX_16;
+  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2;
+  static constexpr int A_STAGE = NL * A_LIMB_BYTES;
+  static constexpr int B_STAGE = NL * B_LIMB_BYTES;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
+  static constexpr int OFF_H = OFF_B + STAGES * B_STAGE;
+  static constexpr int OFF_C = OFF_H + 2 * H_BYTES;
+  static constexpr int OFF_BAR = OFF_C + 2 * C_SLOT;
+  static constexpr int TOTAL = OFF_BAR + 512;
+  static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
+  static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
 };
 
 struct TcParams {
-  int64_t N, F, Fp, D, Dp, Dq, K, Np;
+  int64_t N, F, Fp, D, Dp, Dq, K, Kp, Np;
   int Tn, Td, G;
   int64_t T;
   const float* X;          // caller's X (fp64 recheck)
   const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
-  const double* rowtau;    // int8 mode: per-row part of tau (integer units)
-  const double* coltau;    // int8 mode: per-column part of tau
+  const int64_t* rowtau;   // int8 mode: per-row part of tau (units of 2^14)
+  const int64_t* coltau;   // int8 mode: per-column part of tau
+  const uint8_t* Cil;      // [Td][2][Kp*80] bf16 hi/lo C tiles, interleaved K-major
   float* S_part;           // [G][2][BM][K]
   unsigned* cnt;           // [Tn]
   unsigned long long* recheck_count;
@@ -103,37 +122,45 @@ __device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, in
   return s >= 0.0 ? 1.f : -1.f;
 }
 
-template <int MODE, int KT>  // MODE: 0 bf16, 1 tf32, 2 int8x3
+__device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
+  return (t + 1 == t1) || ((t + 1) / Td != t / Td);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
-  constexpr int NL = (MODE == 2) ? 3 : 1;
-  constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;   // element bytes
-  constexpr int KE = KBYTES / ESZ;                            // K elements per stage
+                const TcParams p) {
+  using CF = Cfg<MODE>;
+  constexpr int NL = CF::NL;
+  constexpr int KE = CF::KE;
   constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
   constexpr uint32_t STAGE_TX = NL * (A_LIMB_BYTES + B_LIMB_BYTES);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the swizzled operand tiles
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = smem + SmemLayout::a;
-  uint8_t* sB = smem + SmemLayout::b;
-  float* sC = reinterpret_cast<float*>(smem + SmemLayout::c);
-  float* sRed = reinterpret_cast<float*>(smem + SmemLayout::red);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* empty = bars + STAGES;       // [STAGES]
-  uint64_t* tfull = bars + 2 * STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;          // [2]
-  uint64_t* cfull = tempty + 2;          // [2]
-  uint64_t* cempty = cfull + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+  uint8_t* sA = smem + CF::OFF_A;
+  uint8_t* sB = smem + CF::OFF_B;
+  uint8_t* sH = smem + CF::OFF_H;
+  uint8_t* sC = smem + CF::OFF_C;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
+  uint64_t* full = bars;                 // [STAGES] operands landed
+  uint64_t* empty = bars + STAGES;       // [STAGES] operands consumed
+  uint64_t* tfull = bars + 2 * STAGES;   // [2] Stage I accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] Stage I accumulator drained
+  uint64_t* cfull = tempty + 2;          // [2] C tile landed
+  uint64_t* cempty = cfull + 2;          // [2] C tile consumed (Stage II MMA done)
+  uint64_t* hfull = cempty + 2;          // [2] H tile written
+  uint64_t* hempty = hfull + 2;          // [2] H tile consumed
+  uint64_t* sfull = hempty + 2;          // [1] Stage II accumulator of a run complete
+  uint64_t* sempty = sfull + 1;          // [1] Stage II accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 1);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int64_t t0 = range_begin(c, p.T, p.G), t1 = range_begin(c + 1, p.T, p.G);
   const int KB = (int)(p.Fp / KE);
+  const uint32_t c_tile_bytes = (uint32_t)(2 * p.Kp * BN * 2);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -144,14 +171,17 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, NUM_EPI);
       mbar_init(cfull + b, 1);
-      mbar_init(cempty + b, NUM_EPI);
+      mbar_init(cempty + b, 1);
+      mbar_init(hfull + b, NUM_EPI);
+      mbar_init(hempty + b, 1);
     }
+    mbar_init(sfull, 1);
+    mbar_init(sempty, NUM_EPI / 2);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmC);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -162,15 +192,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 0) {
     // ===================================================== TMA producer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int cs = 0;
-      uint32_t cphase = 0;
+      int stage = 0, cs = 0;
+      uint32_t phase = 0, cphase = 0;
       for (int64_t t = t0; t < t1; ++t) {
         const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
         mbar_wait(cempty + cs, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull + cs, (uint32_t)(p.K * BN * 4));
-        tma_load_2d(sC + cs * (C_SLOT_BYTES / 4), &tmC, cfull + cs, di * BN, 0);
+        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes);
+        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
         cs ^= 1;
         if (cs == 0) cphase ^= 1;
         for (int kb = 0; kb < KB; ++kb) {
@@ -178,9 +206,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           mbar_arrive_expect_tx(full + stage, STAGE_TX);
 #pragma unroll
           for (int l = 0; l < NL; ++l) {
-            tma_load_2d(sA + stage * A_STAGE_BYTES + l * A_LIMB_BYTES, &tmA, full + stage, kb * KE,
+            tma_load_2d(sA + stage * CF::A_STAGE + l * A_LIMB_BYTES, &tmA, full + stage, kb * KE,
                         (int)(l * p.Np + (int64_t)ni * BM));
-            tma_load_2d(sB + stage * B_STAGE_BYTES + l * B_LIMB_BYTES, &tmB, full + stage, kb * KE,
+            tma_load_2d(sB + stage * CF::B_STAGE + l * B_LIMB_BYTES, &tmB, full + stage, kb * KE,
                         (int)(l * p.Dq + (int64_t)di * BN));
           }
           if (++stage == STAGES) {
@@ -193,22 +221,54 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   } else if (warp == 1) {
     // ===================================================== MMA issuer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int buf = 0;
-      uint32_t bphase = 0;
+      int stage = 0, buf = 0, hb = 0, cs = 0;
+      uint32_t phase = 0, bphase = 0, hphase = 0, cphase = 0, sphase = 0;
+      bool seg_first = true;
+      const uint32_t IDESC2 = make_idesc<0>(BM, (int)p.Kp);
+      const uint32_t d2 = tmem_base + CF::D2_COL;
+      // Stage II for tile tt: S += H(tt) [Chi(tt) + Clo(tt)]^T
+      auto stage2 = [&](int64_t tt) {
+        mbar_wait(hfull + hb, hphase);
+        mbar_wait(cfull + cs, cphase);
+        if (seg_first) mbar_wait(sempty, sphase ^ 1);   // previous run's S drained
+        tc_fence_after();
+        const uint32_t h_base = smem_u32(sH + hb * H_BYTES);
+        const uint32_t c_base = smem_u32(sC + cs * CF::C_SLOT);
+#pragma unroll
+        for (int s = 0; s < BN / 16; ++s) {
+          const uint64_t ad = smem_desc_interleaved(h_base + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const uint64_t bd = smem_desc_interleaved(
+                c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
+            tc_mma<0>(d2, ad, bd, IDESC2, (seg_first && s == 0 && part == 0) ? 0u : 1u);
+          }
+        }
+        seg_first = false;
+        tc_commit(hempty + hb);
+        tc_commit(cempty + cs);
+        if (seg_last(tt, t1, p.Td)) {
+          tc_commit(sfull);
+          seg_first = true;
+          sphase ^= 1;
+        }
+        hb ^= 1;
+        if (hb == 0) hphase ^= 1;
+        cs ^= 1;
+        if (cs == 0) cphase ^= 1;
+      };
       for (int64_t t = t0; t < t1; ++t) {
         mbar_wait(tempty + buf, bphase ^ 1);
         tc_fence_after();
-        const uint32_t acc0 = tmem_base + buf * ACC_BUF_COLS;
+        const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+          const uint32_t a_base = smem_u32(sA + stage * CF::A_STAGE);
+          const uint32_t b_base = smem_u32(sB + stage * CF::B_STAGE);
 #pragma unroll
           for (int ks = 0; ks < KBYTES / 32; ++ks) {
-            const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
+            const uint32_t acc = (kb == 0 && ks == 0) ? 0u : 1u;
             if constexpr (MODE == 2) {
               uint64_t a[3], b[3];
 #pragma unroll
@@ -217,27 +277,29 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 b[l] = smem_desc_sw64(b_base + l * B_LIMB_BYTES + ks * 32);
               }
               // A0 += x0 b0 ; A1 += x0 b1 + x1 b0 ; A2 += x0 b2 + x1 b1 + x2 b0
-              tc_mma<2>(acc0 + 0 * BN, a[0], b[0], IDESC, first);
-              tc_mma<2>(acc0 + 1 * BN, a[0], b[1], IDESC, first);
+              tc_mma<2>(acc0 + 0 * BN, a[0], b[0], IDESC, acc);
+              tc_mma<2>(acc0 + 1 * BN, a[0], b[1], IDESC, acc);
               tc_mma<2>(acc0 + 1 * BN, a[1], b[0], IDESC, 1u);
-              tc_mma<2>(acc0 + 2 * BN, a[0], b[2], IDESC, first);
+              tc_mma<2>(acc0 + 2 * BN, a[0], b[2], IDESC, acc);
               tc_mma<2>(acc0 + 2 * BN, a[1], b[1], IDESC, 1u);
               tc_mma<2>(acc0 + 2 * BN, a[2], b[0], IDESC, 1u);
             } else {
               tc_mma<MODE>(acc0, smem_desc_sw64(a_base + ks * 32), smem_desc_sw64(b_base + ks * 32),
-                           IDESC, first);
+                           IDESC, acc);
             }
           }
-          tc_commit(empty + stage);          // frees the smem stage when these MMAs finish
+          tc_commit(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull + buf);              // accumulators of this tile are ready
+        tc_commit(tfull + buf);
         buf ^= 1;
         if (buf == 0) bphase ^= 1;
+        if (t > t0) stage2(t - 1);          // overlaps the epilogue of tile t-1 with Stage I of t
       }
+      if (t1 > t0) stage2(t1 - 1);
     }
   } else if (warp >= EPI_WARP0) {
     // ===================================================== epilogue
@@ -246,30 +308,31 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int half = ew >> 2;               // column half of the 80-wide tile
     const int m = q * 32 + lane;            // row within the N-tile
     const int K = (int)p.K;
-    float S[KT];
-#pragma unroll
-    for (int k = 0; k < KT; ++k) S[k] = 0.f;
-    int buf = 0;
-    uint32_t bphase = 0;
-    int cs = 0;
-    uint32_t cphase = 0;
+    int buf = 0, hb = 0;
+    uint32_t bphase = 0, hphase = 0, sphase = 0;
     unsigned long long nrecheck = 0;
     const int first_ni = (int)(t0 / p.Td);
     for (int64_t t = t0; t < t1; ++t) {
       const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
       const int64_t row = (int64_t)ni * BM + m;
       const bool row_ok = row < p.N;
-      double rtau = 0.0;
-      if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : 0.0;
+      int64_t rtau = 0, ctau_lo = 0, ctau_hi = 0;
+      if constexpr (MODE == 2) {
+        rtau = row_ok ? __ldg(p.rowtau + row) : 0;
+        const int64_t dbase = (int64_t)di * BN + half * HALF;
+        ctau_lo = __ldg(p.coltau + dbase + lane);
+        ctau_hi = lane < HALF - 32 ? __ldg(p.coltau + dbase + 32 + lane) : 0;
+      }
       mbar_wait(tfull + buf, bphase);
+      mbar_wait(hempty + hb, hphase ^ 1);
       tc_fence_after();
-      mbar_wait(cfull + cs, cphase);
-      const float* cslot = sC + cs * (C_SLOT_BYTES / 4);
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * ACC_BUF_COLS + half * HALF;
+      uint8_t* hrow = sH + hb * H_BYTES + (m >> 3) * CORE_SBO + (m & 7) * 16;
+      const uint32_t tbase =
+          tmem_base + ((uint32_t)(q * 32) << 16) + buf * CF::ACC_STRIDE + half * HALF;
 #pragma unroll 1
       for (int ch = 0; ch < HALF / 8; ++ch) {
         const int col0 = half * HALF + ch * 8;      // column within the tile
-        float h[8];
+        uint32_t hbits = 0;                          // bit j set -> h = -1
         if constexpr (MODE == 2) {
           uint32_t r0[8], r1[8], r2[8];
           tmem_ld8(tbase + ch * 8, r0);
@@ -280,17 +343,19 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           for (int j = 0; j < 8; ++j) {
             const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
                               (int64_t)(int32_t)r2[j];
-            h[j] = I >= 0 ? 1.f : -1.f;
+            if (I < 0) hbits |= 1u << j;
+            const int cj = ch * 8 + j;               // column within this warp's half
+            const int64_t ct = __shfl_sync(0xffffffffu, cj < 32 ? ctau_lo : ctau_hi, cj & 31);
             const int64_t d = (int64_t)di * BN + col0 + j;
-            const bool flag = row_ok && d < p.D &&
-                              fabs((double)I) <= rtau + __ldg(p.coltau + d);
+            const int64_t aI = I < 0 ? -I : I;
+            const bool flag = row_ok && d < p.D && aI <= rtau + ct;
             unsigned mask = __ballot_sync(0xffffffffu, flag);
             while (mask) {
               const int src = __ffs(mask) - 1;
               mask &= mask - 1;
               const int64_t srow = (int64_t)ni * BM + q * 32 + src;
               const float hv = recheck_warp(p, srow, d, lane);
-              if (lane == src) h[j] = hv;
+              if (lane == src) hbits = hv < 0.f ? (hbits | (1u << j)) : (hbits & ~(1u << j));
               ++nrecheck;
             }
           }
@@ -299,99 +364,99 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           tmem_ld8(tbase + ch * 8, r0);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) h[j] = hardsign(__uint_as_float(r0[j]));
+          for (int j = 0; j < 8; ++j)
+            if (!(__uint_as_float(r0[j]) >= 0.f)) hbits |= 1u << j;   // HardSign
         }
-        // Stage II: S[k] += h[c] * C[k, d0 + c]  (padded columns have C = 0)
+        // 8 bf16 +-1 values (0x3F80 / 0xBF80) -> one 16-byte core-matrix row
+        uint32_t w[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-#pragma unroll
-          for (int k = 0; k < KT; ++k)
-            if (k < K) S[k] = fmaf(h[j], cslot[k * BN + col0 + j], S[k]);
-        }
+        for (int j = 0; j < 4; ++j)
+          w[j] = (((hbits >> (2 * j)) & 1u) ? 0xBF80u : 0x3F80u) |
+                 ((((hbits >> (2 * j + 1)) & 1u) ? 0xBF80u : 0x3F80u) << 16);
+        *reinterpret_cast<uint4*>(hrow + (col0 >> 3) * CORE_LBO) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      // release the TMEM buffer and the C slot
       tc_fence_before();
+      fence_proxy_async_smem();      // H writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(tempty + buf);
-        mbar_arrive(cempty + cs);
+        mbar_arrive(hfull + hb);
       }
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
-      cs ^= 1;
-      if (cs == 0) cphase ^= 1;
+      hb ^= 1;
+      if (hb == 0) hphase ^= 1;
 
-      // ---- end of this CTA's run of D-tiles for N-tile ni?
-      const bool seg_end = (t + 1 == t1) || ((t + 1) / p.Td != ni);
-      if (!seg_end) continue;
-      // combine the two column halves (fixed order: half 0 + half 1)
-      if (half == 1) {
-#pragma unroll
-        for (int k = 0; k < KT; ++k)
-          if (k < K) sRed[k * BM + m] = S[k];
-      }
-      named_bar(1, NUM_EPI * 32);
+      if (!seg_last(t, t1, p.Td)) continue;
+      // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM
       const int c_first = owner_of((int64_t)ni * p.Td, p.T, p.G);
       const int c_last = owner_of((int64_t)(ni + 1) * p.Td - 1, p.T, p.G);
       const bool sole = (c_first == c_last);
       if (half == 0) {
+        mbar_wait(sfull, sphase);
+        tc_fence_after();
+        const uint32_t sb = tmem_base + ((uint32_t)(q * 32) << 16) + CF::D2_COL;
+        float* part = p.S_part + (((int64_t)c * 2 + ((ni == first_ni) ? 0 : 1)) * BM + m) * p.K;
+        int best = 0;
+        float bv = 0.f;
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          uint32_t r[8];
+          tmem_ld8(sb + k0, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < KT; ++k)
-          if (k < K) S[k] = S[k] + sRed[k * BM + m];
-        if (!sole) {
-          const int slot = (ni == first_ni) ? 0 : 1;
-          float* part = p.S_part + (((int64_t)c * 2 + slot) * BM + m) * p.K;
-#pragma unroll
-          for (int k = 0; k < KT; ++k)
-            if (k < K) part[k] = S[k];
-          __threadfence();
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            if (k < K) {
+              const float v = __uint_as_float(r[j]);
+              if (sole) {
+                if (row_ok && p.scores) p.scores[row * p.K + k] = v;
+                if (k == 0 || v > bv) {
+                  bv = v;
+                  best = k;
+                }
+              } else {
+                part[k] = v;
+              }
+            }
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty);
+        if (sole && row_ok && p.labels) p.labels[row] = best;
+        if (!sole) __threadfence();
       }
+      sphase ^= 1;
+      if (sole) continue;
       named_bar(1, NUM_EPI * 32);
-      if (!sole && threadIdx.x == EPI_WARP0 * 32) {
+      if (threadIdx.x == EPI_WARP0 * 32) {
         const unsigned prev = atomicAdd(p.cnt + ni, 1u);
         *s_flag = (prev == (unsigned)(c_last - c_first)) ? 1 : 0;
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      const bool finalize = sole || (*s_flag != 0);
-      if (finalize && half == 0) {
-        if (!sole) {
-          __threadfence();
-#pragma unroll
-          for (int k = 0; k < KT; ++k) S[k] = 0.f;
+      if (*s_flag && half == 0 && row_ok) {
+        __threadfence();
+        int best = 0;
+        float bv = 0.f;
+        for (int k = 0; k < K; ++k) {
+          float s = 0.f;
           for (int cc = c_first; cc <= c_last; ++cc) {
             const int slot = ((int)(range_begin(cc, p.T, p.G) / p.Td) == ni) ? 0 : 1;
-            const float* part = p.S_part + (((int64_t)cc * 2 + slot) * BM + m) * p.K;
-#pragma unroll
-            for (int k = 0; k < KT; ++k)
-              if (k < K) S[k] = (cc == c_first) ? ld_cg(part + k) : S[k] + ld_cg(part + k);
+            const float v = ld_cg(p.S_part + (((int64_t)cc * 2 + slot) * BM + m) * p.K + k);
+            s = (cc == c_first) ? v : s + v;
+          }
+          if (p.scores) p.scores[row * p.K + k] = s;
+          if (k == 0 || s > bv) {
+            bv = s;
+            best = k;
           }
         }
-        if (row_ok) {
-          int best = 0;
-          float bv = S[0];
-#pragma unroll
-          for (int k = 0; k < KT; ++k) {
-            if (k < K) {
-              if (p.scores) p.scores[row * p.K + k] = S[k];
-              if (k > 0 && S[k] > bv) {
-                bv = S[k];
-                best = k;
-              }
-            }
-          }
-          if (p.labels) p.labels[row] = best;
-        }
+        if (p.labels) p.labels[row] = best;
       }
-#pragma unroll
-      for (int k = 0; k < KT; ++k) S[k] = 0.f;
-      named_bar(1, NUM_EPI * 32);   // sRed / s_flag reuse
+      named_bar(1, NUM_EPI * 32);     // s_flag reuse
     }
-    if (MODE == 2) {
-      // one atomic per warp (lane 0 holds the warp's count: all lanes counted the same items)
-      if (lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
-    }
+    if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
   __syncwarp();
   __syncthreads();
@@ -424,7 +489,7 @@ __device__ __forceinline__ float scale_for(float amax) {
 // int8 limbs into out[l][rows_p][Fp] and the per-row tau term.
 __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
                                  int64_t F, int64_t ld_src, int64_t Fp, int8_t* __restrict__ out,
-                                 double* __restrict__ tau_part, double tau_const) {
+                                 int64_t* __restrict__ tau_part, int64_t tau_const) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (r >= rows_p) return;
@@ -448,10 +513,11 @@ __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, in
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
   // |c_x c_b x.b - U_x.U_b| <= 0.625 (L1(U_x) + L1(U_b)) + 0.3907 F and the dropped limb
-  // products (i + j >= 3) add <= F (2^20 + 2^12).  The kernel compares in
-  // units of 2^14 (I = A0 2^14 + A1 2^7 + A2 = U_x.U_b / 2^14 without the dropped terms).
+  // products (i + j >= 3) add <= F (2^20 + 2^12).  The kernel compares
+  // I = A0 2^14 + A1 2^7 + A2 = (U_x.U_b - dropped) / 2^14, so tau is stored / 2^14,
+  // rounded up: ceil((5 l1 / 8 + tau_const) / 2^14) = (5 l1 + 8 tau_const + 2^17 - 1) >> 17.
   if (lane == 0 && tau_part)
-    tau_part[r] = valid ? (0.625 * (double)l1 * (1.0 + 1e-12) + tau_const) * (1.0 / 16384.0) : 0.0;
+    tau_part[r] = valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : 0;
 }
 
 // Rounded copies for the bf16 / tf32 modes: out[r][f] (rows_p x Fp, zero padded).
@@ -470,6 +536,29 @@ __global__ void round_rows_kernel(const float* __restrict__ src, int64_t rows, i
       asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
       reinterpret_cast<uint32_t*>(out)[i] = y;
     }
+  }
+}
+
+
+// C tiles for Stage II: per D-tile di, bf16 hi = RN(C), lo = RN(C - hi), each
+// [Kp][80] in the interleaved K-major core-matrix layout the MMA B descriptor
+// expects (core matrix (g, j) = rows 8g.., columns 8j.. at byte (10 g + j) * 128).
+__global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int64_t Kp, int64_t D,
+                                    int64_t Dp, int64_t Td, __nv_bfloat16* __restrict__ out) {
+  const int64_t per_part = Kp * BN;
+  const int64_t total = Td * 2 * per_part;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t di = i / (2 * per_part);
+    const int part = (int)((i / per_part) % 2);
+    const int64_t e = i % per_part;          // element index inside the interleaved part
+    const int64_t core = e / 64, inner = e % 64;
+    const int64_t g = core / (BN / 8), j = core % (BN / 8);
+    const int64_t r = g * 8 + inner / 8, cc = j * 8 + inner % 8;
+    const int64_t d = di * BN + cc;
+    const float v = (r < K && d < D) ? Cp[r * Dp + d] : 0.f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    out[i] = part == 0 ? hi : __float2bfloat16_rn(v - __bfloat162float(hi));
   }
 }
 
@@ -504,35 +593,30 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int KT>
-cudaError_t launch_mode_kt(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
-                           const TcParams& p, cudaStream_t st) {
-  const size_t sm = SmemLayout::total + 1024;
-  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE, KT>,
+template <int MODE>
+cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t st) {
+  const size_t sm = Cfg<MODE>::TOTAL + 1024;
+  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  fused_tc_kernel<MODE, KT><<<p.G, THREADS, sm, st>>>(a, b, cm, p);
+  fused_tc_kernel<MODE><<<p.G, THREADS, sm, st>>>(a, b, p);
   return cudaGetLastError();
-}
-
-template <int MODE>
-cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cm,
-                        const TcParams& p, cudaStream_t st) {
-  if (p.K <= 8) return launch_mode_kt<MODE, 8>(a, b, cm, p, st);
-  if (p.K <= 16) return launch_mode_kt<MODE, 16>(a, b, cm, p, st);
-  return launch_mode_kt<MODE, 32>(a, b, cm, p, st);
 }
 
 }  // namespace
 
 int tc_tile_n() { return BN; }
-int tc_max_k() { return KT_MAX; }
+int tc_max_k(int mode) { return mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
+int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
 int64_t tc_max_fp_int8() { return 100000; }
 
-double tc_tau_const(int64_t F) { return (double)F * (0.390625 + 1048576.0 + 4096.0) * (1.0 + 1e-12) + 1.0; }
+int64_t tc_tau_const(int64_t F) {
+  // F (0.390625 + 2^20 + 2^12) + 1, in the integer units of U_x.U_b (before the 2^-14 scale)
+  return (int64_t)F * 1052673 + 1;
+}
 
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
-                            int64_t Fp, int8_t* out, double* tau_part, double tau_const,
+                            int64_t Fp, int8_t* out, int64_t* tau_part, int64_t tau_const,
                             cudaStream_t st) {
   const int warps = 8;
   limb_rows_kernel<<<(unsigned)((rows_p + warps - 1) / warps), warps * 32, 0, st>>>(
@@ -552,9 +636,19 @@ cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t ro
   return cudaGetLastError();
 }
 
+cudaError_t launch_tc_c_interleave(const float* Cp, int64_t K, int64_t Kp, int64_t D, int64_t Dp,
+                                   void* out, cudaStream_t st) {
+  const int64_t Td = (D + BN - 1) / BN;
+  const int64_t total = Td * 2 * Kp * BN;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  c_interleave_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, Kp, D, Dp, Td, (__nv_bfloat16*)out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st) {
-  const int64_t Tn = (o.N_p) / BM;
+  const int64_t Tn = o.N_p / BM;
   const int64_t Td = (o.D + BN - 1) / BN;
   TcParams p;
   p.N = N;
@@ -564,6 +658,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.Dp = o.Dp;
   p.Dq = o.Dq;
   p.K = o.K;
+  p.Kp = tc_kp(o.K);
   p.Np = o.N_p;
   p.Tn = (int)Tn;
   p.Td = (int)Td;
@@ -573,6 +668,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.Bt = o.Bt;
   p.rowtau = o.rowtau;
   p.coltau = o.coltau;
+  p.Cil = (const uint8_t*)o.Cil;
   p.S_part = o.S_part;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
@@ -583,17 +679,15 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   const CUtensorMapDataType dt = (mode == 0)   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb;
   if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, KBYTES / esz, BM,
                    CU_TENSOR_MAP_SWIZZLE_64B) ||
       !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, KBYTES / esz, BN,
-                   CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map_2d(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, o.Cp, (uint64_t)o.Dp, (uint64_t)o.K, BN,
-                   (uint32_t)o.K, CU_TENSOR_MAP_SWIZZLE_NONE))
+                   CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  if (mode == 0) return launch_mode<0>(ma, mb, mc, p, st);
-  if (mode == 1) return launch_mode<1>(ma, mb, mc, p, st);
-  return launch_mode<2>(ma, mb, mc, p, st);
+  if (mode == 0) return launch_mode<0>(ma, mb, p, st);
+  if (mode == 1) return launch_mode<1>(ma, mb, p, st);
+  return launch_mode<2>(ma, mb, p, st);
 }
 
 }  // namespace hdc

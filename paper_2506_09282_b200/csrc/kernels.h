@@ -61,24 +61,27 @@ struct TcOperands {
   int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to the 80-column tile; N_p to 128 rows
   const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
   const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
-  const float* Cp;                   // [K][Dp] fp32
+  const void* Cil;                   // [Td][2][Kp*80] bf16 C hi/lo tiles (interleaved)
   const float* X;                    // caller's X (fp64 recheck)
   const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
-  const double* rowtau;              // [N_p] int8 mode
-  const double* coltau;              // [Dq]  int8 mode
+  const int64_t* rowtau;             // [N_p] int8 mode
+  const int64_t* coltau;             // [Dq]  int8 mode
   float* S_part;                     // [num_sms][2][128][K]
   unsigned* cnt;                     // [N_p / 128]
   unsigned long long* recheck;
 };
 int tc_tile_n();
-int tc_max_k();
+int tc_max_k(int mode);
+int64_t tc_kp(int64_t K);
 int64_t tc_max_fp_int8();
-double tc_tau_const(int64_t F);
+int64_t tc_tau_const(int64_t F);
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
-                            int64_t Fp, int8_t* out, double* tau_part, double tau_const,
+                            int64_t Fp, int8_t* out, int64_t* tau_part, int64_t tau_const,
                             cudaStream_t st);
 cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t rows_p, int64_t F,
                             int64_t ld_src, int64_t Fp, void* out, cudaStream_t st);
+cudaError_t launch_tc_c_interleave(const float* Cp, int64_t K, int64_t Kp, int64_t D, int64_t Dp,
+                                   void* out, cudaStream_t st);
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st);
 
