@@ -34,6 +34,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -45,38 +48,41 @@ using namespace ptx;
 
 constexpr int BM = 128;              // rows per tile (MMA M)
 constexpr int BN = 80;               // D columns per tile; 10000 = 125 x 80
-constexpr int KBYTES = 64;           // K bytes per stage (SWIZZLE_64B atom row)
-constexpr int STAGES = 4;
-constexpr int THREADS = 384;
+constexpr int STAGES_MAX = 6;
+constexpr int THREADS = 640;          // 4 role warps + 16 epilogue warps
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI = 8;
-constexpr int HALF = BN / 2;         // columns per epilogue warp
+constexpr int NUM_EPI = 16;
+constexpr int EPI_COLS = BN / 4;     // columns per epilogue warp (4 column quarters)
 constexpr int MAX_LIMBS = 3;
-constexpr int A_LIMB_BYTES = BM * KBYTES;            // 8192
-constexpr int B_LIMB_BYTES = BN * KBYTES;            // 5120
-constexpr int A_STAGE_BYTES = MAX_LIMBS * A_LIMB_BYTES;
-constexpr int B_STAGE_BYTES = MAX_LIMBS * B_LIMB_BYTES;
 constexpr int H_BYTES = BM * BN * 2;                 // bf16 H tile (interleaved K-major)
 constexpr int CORE_LBO = 128;                        // K-adjacent 8x16B core matrices
 constexpr int CORE_SBO = (BN / 8) * 128;             // 8-row groups (10 core matrices)
 constexpr int KP_MAX_I8 = 32;                        // Stage II N (classes) limits
-constexpr int KP_MAX_16 = 128;
+constexpr int KP_MAX_16 = 64;
 constexpr int C_SLOT_MAX = 2 * KP_MAX_16 * BN * 2;   // bf16 hi + lo, [Kp][80] each
 
 template <int MODE>
 struct Cfg {
   static constexpr int NL = (MODE == 2) ? 3 : 1;
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
+  // K bytes per stage = one swizzle-atom row: 128 B (SWIZZLE_128B) for the single-operand
+  // modes, 64 B (SWIZZLE_64B) for the 3-limb int8 mode (smem budget).
+  static constexpr int KBYTES = (MODE == 2) ? 64 : 128;
+  static constexpr int SWZ = (MODE == 2) ? 4 : 2;                // descriptor layout type
+  static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
+  static constexpr int A_LIMB_BYTES = BM * KBYTES;
+  static constexpr int B_LIMB_BYTES = BN * KBYTES;
   static constexpr int KE = KBYTES / ESZ;                      // K elements per stage
   static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : 128;  // TMEM cols per Stage I buffer
   static constexpr int D2_COL = (MODE == 2) ? 480 : 256;          // Stage II accumulator
   static constexpr int KP_MAX = (MODE == 2) ? KP_MAX_I8 : KP_MAX_16;
-  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2;
+  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + BN * 8;   // + int64 column taus (int8)
+  static constexpr int STAGES_ = (MODE == 2) ? 4 : 5;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
   static constexpr int OFF_A = 0;
-  static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
-  static constexpr int OFF_H = OFF_B + STAGES * B_STAGE;
+  static constexpr int OFF_B = OFF_A + STAGES_ * A_STAGE;
+  static constexpr int OFF_H = OFF_B + STAGES_ * B_STAGE;
   static constexpr int OFF_C = OFF_H + 2 * H_BYTES;
   static constexpr int OFF_BAR = OFF_C + 2 * C_SLOT;
   static constexpr int TOTAL = OFF_BAR + 512;
@@ -98,7 +104,22 @@ struct TcParams {
   unsigned long long* recheck_count;
   float* scores;
   int32_t* labels;
+  int debug;               // diagnostics only (HDC_TC_DEBUG): 1 = no Stage I MMA, 2 = no operand TMA,
+                           // 4 = per-role wait-cycle counters into dbg[]
+  unsigned long long* dbg; // [16] cycle counters (debug & 4)
 };
+
+// Timed barrier wait (diagnostics): accumulates the cycles spent waiting.
+#define TWAIT(slot, bar, par)                                        \
+  do {                                                               \
+    if (p.debug & 4) {                                               \
+      const long long _t0 = clock64();                               \
+      mbar_wait(bar, par);                                           \
+      dbgc[slot] += (unsigned long long)(clock64() - _t0);           \
+    } else {                                                         \
+      mbar_wait(bar, par);                                           \
+    }                                                                \
+  } while (0)
 
 __device__ __forceinline__ int64_t range_begin(int c, int64_t T, int G) { return (int64_t)c * T / G; }
 __device__ __forceinline__ int owner_of(int64_t t, int64_t T, int G) {
@@ -134,7 +155,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   constexpr int NL = CF::NL;
   constexpr int KE = CF::KE;
   constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
-  constexpr uint32_t STAGE_TX = NL * (A_LIMB_BYTES + B_LIMB_BYTES);
+  constexpr uint32_t IDESC_N160 = make_idesc<MODE>(BM, 2 * BN);
+  constexpr uint32_t IDESC_N240 = make_idesc<MODE>(BM, 3 * BN);
+  constexpr uint32_t STAGE_TX = NL * (CF::A_LIMB_BYTES + CF::B_LIMB_BYTES);
+  constexpr int A_LIMB_BYTES = CF::A_LIMB_BYTES;
+  constexpr int KBYTES = CF::KBYTES;
+  constexpr int STAGES = CF::STAGES_;
+  auto sdesc = [](uint32_t addr) { return smem_desc_sw(addr, CF::SBO, CF::SWZ); };
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -160,6 +187,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const int c = blockIdx.x;
   const int64_t t0 = range_begin(c, p.T, p.G), t1 = range_begin(c + 1, p.T, p.G);
   const int KB = (int)(p.Fp / KE);
+  unsigned long long dbgc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) dbgc[i] = 0;
+  const long long t_start = clock64();
   const uint32_t c_tile_bytes = (uint32_t)(2 * p.Kp * BN * 2);
 
   if (threadIdx.x == 0) {
@@ -176,7 +207,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(hempty + b, 1);
     }
     mbar_init(sfull, 1);
-    mbar_init(sempty, NUM_EPI / 2);
+    mbar_init(sempty, 4);               // the 4 warps of column quarter 0 drain S
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -190,25 +221,28 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================================================== TMA producer
+    // ===================================================== TMA producer (operands)
     if (lane == 0) {
-      int stage = 0, cs = 0;
-      uint32_t phase = 0, cphase = 0;
+      int stage = 0;
+      uint32_t phase = 0;
       for (int64_t t = t0; t < t1; ++t) {
         const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
-        mbar_wait(cempty + cs, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes);
-        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
-        cs ^= 1;
-        if (cs == 0) cphase ^= 1;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
+          TWAIT(0, empty + stage, phase ^ 1);
+          if (p.debug & 2) {
+            mbar_arrive(full + stage);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(full + stage, STAGE_TX);
 #pragma unroll
           for (int l = 0; l < NL; ++l) {
             tma_load_2d(sA + stage * CF::A_STAGE + l * A_LIMB_BYTES, &tmA, full + stage, kb * KE,
                         (int)(l * p.Np + (int64_t)ni * BM));
-            tma_load_2d(sB + stage * CF::B_STAGE + l * B_LIMB_BYTES, &tmB, full + stage, kb * KE,
+            tma_load_2d(sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES, &tmB, full + stage, kb * KE,
                         (int)(l * p.Dq + (int64_t)di * BN));
           }
           if (++stage == STAGES) {
@@ -218,9 +252,27 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================================================== MMA issuer
+  } else if (warp == 2) {
+    // ===================================================== C-tile producer (Stage II B operand)
+    // A separate warp, so the operand stream never waits for a C slot.
     if (lane == 0) {
+      int cs = 0;
+      uint32_t cphase = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        const int di = (int)(t % p.Td);
+        mbar_wait(cempty + cs, cphase ^ 1);
+        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));
+        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
+        if constexpr (MODE == 2)
+          bulk_load(sC + cs * CF::C_SLOT + CF::C_SLOT - BN * 8, p.coltau + (int64_t)di * BN, BN * 8,
+                    cfull + cs);
+        cs ^= 1;
+        if (cs == 0) cphase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer (whole warp, elected lane issues)
+    {
       int stage = 0, buf = 0, hb = 0, cs = 0;
       uint32_t phase = 0, bphase = 0, hphase = 0, cphase = 0, sphase = 0;
       bool seg_first = true;
@@ -228,9 +280,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint32_t d2 = tmem_base + CF::D2_COL;
       // Stage II for tile tt: S += H(tt) [Chi(tt) + Clo(tt)]^T
       auto stage2 = [&](int64_t tt) {
-        mbar_wait(hfull + hb, hphase);
-        mbar_wait(cfull + cs, cphase);
-        if (seg_first) mbar_wait(sempty, sphase ^ 1);   // previous run's S drained
+        TWAIT(3, hfull + hb, hphase);
+        TWAIT(4, cfull + cs, cphase);
+        if (seg_first) TWAIT(5, sempty, sphase ^ 1);   // previous run's S drained
         tc_fence_after();
         const uint32_t h_base = smem_u32(sH + hb * H_BYTES);
         const uint32_t c_base = smem_u32(sC + cs * CF::C_SLOT);
@@ -241,14 +293,14 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           for (int part = 0; part < 2; ++part) {
             const uint64_t bd = smem_desc_interleaved(
                 c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
-            tc_mma<0>(d2, ad, bd, IDESC2, (seg_first && s == 0 && part == 0) ? 0u : 1u);
+            if (!(p.debug & 8)) tc_mma_elect<0>(d2, ad, bd, IDESC2, (seg_first && s == 0 && part == 0) ? 0u : 1u);
           }
         }
         seg_first = false;
-        tc_commit(hempty + hb);
-        tc_commit(cempty + cs);
+        tc_commit_elect(hempty + hb);
+        tc_commit_elect(cempty + cs);
         if (seg_last(tt, t1, p.Td)) {
-          tc_commit(sfull);
+          tc_commit_elect(sfull);
           seg_first = true;
           sphase ^= 1;
         }
@@ -258,43 +310,40 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (cs == 0) cphase ^= 1;
       };
       for (int64_t t = t0; t < t1; ++t) {
-        mbar_wait(tempty + buf, bphase ^ 1);
+        TWAIT(1, tempty + buf, bphase ^ 1);
         tc_fence_after();
         const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(full + stage, phase);
+          TWAIT(2, full + stage, phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * CF::A_STAGE);
           const uint32_t b_base = smem_u32(sB + stage * CF::B_STAGE);
 #pragma unroll
-          for (int ks = 0; ks < KBYTES / 32; ++ks) {
+          for (int ks = 0; ks < ((p.debug & 1) ? 0 : KBYTES / 32); ++ks) {
             const uint32_t acc = (kb == 0 && ks == 0) ? 0u : 1u;
             if constexpr (MODE == 2) {
-              uint64_t a[3], b[3];
-#pragma unroll
-              for (int l = 0; l < 3; ++l) {
-                a[l] = smem_desc_sw64(a_base + l * A_LIMB_BYTES + ks * 32);
-                b[l] = smem_desc_sw64(b_base + l * B_LIMB_BYTES + ks * 32);
-              }
-              // A0 += x0 b0 ; A1 += x0 b1 + x1 b0 ; A2 += x0 b2 + x1 b1 + x2 b0
-              tc_mma<2>(acc0 + 0 * BN, a[0], b[0], IDESC, acc);
-              tc_mma<2>(acc0 + 1 * BN, a[0], b[1], IDESC, acc);
-              tc_mma<2>(acc0 + 1 * BN, a[1], b[0], IDESC, 1u);
-              tc_mma<2>(acc0 + 2 * BN, a[0], b[2], IDESC, acc);
-              tc_mma<2>(acc0 + 2 * BN, a[1], b[1], IDESC, 1u);
-              tc_mma<2>(acc0 + 2 * BN, a[2], b[0], IDESC, 1u);
+              // The three B limb tiles are contiguous rows [b0; b1; b2] (240 x 64 B) and
+              // the accumulators contiguous columns [A0 | A1 | A2], so one MMA per A limb:
+              //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
+              // (each A tile is read from shared memory once per k-step, not 3 times).
+              const uint64_t bdesc = sdesc(b_base + ks * 32);
+              tc_mma_elect<2>(acc0, sdesc(a_base + ks * 32), bdesc, IDESC_N240, acc);
+              tc_mma_elect<2>(acc0 + BN, sdesc(a_base + A_LIMB_BYTES + ks * 32), bdesc,
+                        IDESC_N160, 1u);
+              tc_mma_elect<2>(acc0 + 2 * BN, sdesc(a_base + 2 * A_LIMB_BYTES + ks * 32), bdesc,
+                        IDESC, 1u);
             } else {
-              tc_mma<MODE>(acc0, smem_desc_sw64(a_base + ks * 32), smem_desc_sw64(b_base + ks * 32),
+              tc_mma_elect<MODE>(acc0, sdesc(a_base + ks * 32), sdesc(b_base + ks * 32),
                            IDESC, acc);
             }
           }
-          tc_commit(empty + stage);
+          tc_commit_elect(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull + buf);
+        tc_commit_elect(tfull + buf);
         buf ^= 1;
         if (buf == 0) bphase ^= 1;
         if (t > t0) stage2(t - 1);          // overlaps the epilogue of tile t-1 with Stage I of t
@@ -304,76 +353,78 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   } else if (warp >= EPI_WARP0) {
     // ===================================================== epilogue
     const int ew = warp - EPI_WARP0;
-    const int q = warp & 3;                 // TMEM lane quarter
-    const int half = ew >> 2;               // column half of the 80-wide tile
+    const int q = warp & 3;                 // TMEM lane quarter (hardware: warp id % 4)
+    const int cq = ew >> 2;                 // column quarter of the 80-wide tile
     const int m = q * 32 + lane;            // row within the N-tile
     const int K = (int)p.K;
-    int buf = 0, hb = 0;
-    uint32_t bphase = 0, hphase = 0, sphase = 0;
+    int buf = 0, hb = 0, cs = 0;
+    uint32_t bphase = 0, hphase = 0, sphase = 0, cphase = 0;
     unsigned long long nrecheck = 0;
     const int first_ni = (int)(t0 / p.Td);
     for (int64_t t = t0; t < t1; ++t) {
       const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
       const int64_t row = (int64_t)ni * BM + m;
       const bool row_ok = row < p.N;
-      int64_t rtau = 0, ctau_lo = 0, ctau_hi = 0;
+      int64_t rtau = -1;                    // int8 mode: row part of tau (-1: padded row, never flag)
+      if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : -(int64_t(1) << 62);
+      TWAIT(6, tfull + buf, bphase);
+      TWAIT(7, hempty + hb, hphase ^ 1);
+      const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
       if constexpr (MODE == 2) {
-        rtau = row_ok ? __ldg(p.rowtau + row) : 0;
-        const int64_t dbase = (int64_t)di * BN + half * HALF;
-        ctau_lo = __ldg(p.coltau + dbase + lane);
-        ctau_hi = lane < HALF - 32 ? __ldg(p.coltau + dbase + 32 + lane) : 0;
+        mbar_wait(cfull + cs, cphase);
+        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + CF::C_SLOT - BN * 8);
       }
-      mbar_wait(tfull + buf, bphase);
-      mbar_wait(hempty + hb, hphase ^ 1);
       tc_fence_after();
       uint8_t* hrow = sH + hb * H_BYTES + (m >> 3) * CORE_SBO + (m & 7) * 16;
       const uint32_t tbase =
-          tmem_base + ((uint32_t)(q * 32) << 16) + buf * CF::ACC_STRIDE + half * HALF;
+          tmem_base + ((uint32_t)(q * 32) << 16) + buf * CF::ACC_STRIDE + cq * EPI_COLS;
 #pragma unroll 1
-      for (int ch = 0; ch < HALF / 8; ++ch) {
-        const int col0 = half * HALF + ch * 8;      // column within the tile
-        uint32_t hbits = 0;                          // bit j set -> h = -1
+      for (int ch = 0; ch < ((p.debug & 16) ? 0 : EPI_COLS / 4); ++ch) {
+        const int col0 = cq * EPI_COLS + ch * 4;   // column within the tile
+        uint32_t hbits = 0;                         // bit j set -> h = -1
         if constexpr (MODE == 2) {
-          uint32_t r0[8], r1[8], r2[8];
-          tmem_ld8(tbase + ch * 8, r0);
-          tmem_ld8(tbase + BN + ch * 8, r1);
-          tmem_ld8(tbase + 2 * BN + ch * 8, r2);
+          uint32_t r0[4], r1[4], r2[4];
+          tmem_ld4(tbase + ch * 4, r0);
+          tmem_ld4(tbase + BN + ch * 4, r1);
+          tmem_ld4(tbase + 2 * BN + ch * 4, r2);
           tmem_ld_wait();
+          int64_t I[4];
+          uint32_t fl = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
-                              (int64_t)(int32_t)r2[j];
-            if (I < 0) hbits |= 1u << j;
-            const int cj = ch * 8 + j;               // column within this warp's half
-            const int64_t ct = __shfl_sync(0xffffffffu, cj < 32 ? ctau_lo : ctau_hi, cj & 31);
-            const int64_t d = (int64_t)di * BN + col0 + j;
-            const int64_t aI = I < 0 ? -I : I;
-            const bool flag = row_ok && d < p.D && aI <= rtau + ct;
-            unsigned mask = __ballot_sync(0xffffffffu, flag);
-            while (mask) {
-              const int src = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const int64_t srow = (int64_t)ni * BM + q * 32 + src;
-              const float hv = recheck_warp(p, srow, d, lane);
-              if (lane == src) hbits = hv < 0.f ? (hbits | (1u << j)) : (hbits & ~(1u << j));
-              ++nrecheck;
+          for (int j = 0; j < 4; ++j) {
+            I[j] = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
+                   (int64_t)(int32_t)r2[j];
+            if (I[j] < 0) hbits |= 1u << j;
+            const int64_t aI = I[j] < 0 ? -I[j] : I[j];
+            if (aI <= rtau + sct[col0 + j]) fl |= 1u << j;   // coltau = -inf past D
+          }
+          if (__any_sync(0xffffffffu, fl != 0)) {
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {
+              unsigned mask = __ballot_sync(0xffffffffu, (fl >> j) & 1u);
+              const int64_t d = (int64_t)di * BN + col0 + j;
+              while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int64_t srow = (int64_t)ni * BM + q * 32 + src;
+                const float hv = recheck_warp(p, srow, d, lane);
+                if (lane == src) hbits = hv < 0.f ? (hbits | (1u << j)) : (hbits & ~(1u << j));
+                ++nrecheck;
+              }
             }
           }
         } else {
-          uint32_t r0[8];
-          tmem_ld8(tbase + ch * 8, r0);
+          uint32_t r0[4];
+          tmem_ld4(tbase + ch * 4, r0);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < 4; ++j)
             if (!(__uint_as_float(r0[j]) >= 0.f)) hbits |= 1u << j;   // HardSign
         }
-        // 8 bf16 +-1 values (0x3F80 / 0xBF80) -> one 16-byte core-matrix row
-        uint32_t w[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          w[j] = (((hbits >> (2 * j)) & 1u) ? 0xBF80u : 0x3F80u) |
-                 ((((hbits >> (2 * j + 1)) & 1u) ? 0xBF80u : 0x3F80u) << 16);
-        *reinterpret_cast<uint4*>(hrow + (col0 >> 3) * CORE_LBO) = make_uint4(w[0], w[1], w[2], w[3]);
+        // 4 bf16 +-1 values (0x3F80 / 0xBF80) -> 8 bytes of a core-matrix row
+        const uint32_t w0 = ((hbits & 1u) ? 0xBF80u : 0x3F80u) | (((hbits & 2u) ? 0xBF80u : 0x3F80u) << 16);
+        const uint32_t w1 = ((hbits & 4u) ? 0xBF80u : 0x3F80u) | (((hbits & 8u) ? 0xBF80u : 0x3F80u) << 16);
+        *reinterpret_cast<uint2*>(hrow + (col0 >> 3) * CORE_LBO + (col0 & 7) * 2) = make_uint2(w0, w1);
       }
       tc_fence_before();
       fence_proxy_async_smem();      // H writes -> visible to the tensor core
@@ -386,14 +437,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (buf == 0) bphase ^= 1;
       hb ^= 1;
       if (hb == 0) hphase ^= 1;
+      cs ^= 1;
+      if (cs == 0) cphase ^= 1;
 
       if (!seg_last(t, t1, p.Td)) continue;
       // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM
       const int c_first = owner_of((int64_t)ni * p.Td, p.T, p.G);
       const int c_last = owner_of((int64_t)(ni + 1) * p.Td - 1, p.T, p.G);
       const bool sole = (c_first == c_last);
-      if (half == 0) {
-        mbar_wait(sfull, sphase);
+      if (cq == 0) {
+        TWAIT(8, sfull, sphase);
         tc_fence_after();
         const uint32_t sb = tmem_base + ((uint32_t)(q * 32) << 16) + CF::D2_COL;
         float* part = p.S_part + (((int64_t)c * 2 + ((ni == first_ni) ? 0 : 1)) * BM + m) * p.K;
@@ -435,7 +488,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      if (*s_flag && half == 0 && row_ok) {
+      if (*s_flag && cq == 0 && row_ok) {
         __threadfence();
         int best = 0;
         float bv = 0.f;
@@ -457,6 +510,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       named_bar(1, NUM_EPI * 32);     // s_flag reuse
     }
     if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
+  }
+  if ((p.debug & 4) && lane == 0 && (warp <= 2 || warp == EPI_WARP0)) {
+    dbgc[9 + (warp == EPI_WARP0 ? 3 : warp)] = (unsigned long long)(clock64() - t_start);
+    for (int i = 0; i < 16; ++i)
+      if (dbgc[i]) atomicAdd(p.dbg + i, dbgc[i]);
   }
   __syncwarp();
   __syncthreads();
@@ -517,7 +575,7 @@ __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, in
   // I = A0 2^14 + A1 2^7 + A2 = (U_x.U_b - dropped) / 2^14, so tau is stored / 2^14,
   // rounded up: ceil((5 l1 / 8 + tau_const) / 2^14) = (5 l1 + 8 tau_const + 2^17 - 1) >> 17.
   if (lane == 0 && tau_part)
-    tau_part[r] = valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : 0;
+    tau_part[r] = valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : -(int64_t(1) << 62);
 }
 
 // Rounded copies for the bf16 / tf32 modes: out[r][f] (rows_p x Fp, zero padded).
@@ -674,20 +732,45 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.recheck_count = o.recheck;
   p.scores = scores;
   p.labels = labels;
+  {
+    const char* dbg = getenv("HDC_TC_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
+  static unsigned long long* dbg_buf = nullptr;
+  p.dbg = nullptr;
+  if (p.debug & 4) {
+    if (!dbg_buf) cudaMalloc((void**)&dbg_buf, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_buf, 0, 16 * sizeof(unsigned long long), st);
+    p.dbg = dbg_buf;
+  }
   const int nl = (mode == 2) ? 3 : 1;
   const int esz = (mode == 0) ? 2 : (mode == 1) ? 4 : 1;
   const CUtensorMapDataType dt = (mode == 0)   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUtensorMap ma, mb;
-  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, KBYTES / esz, BM,
-                   CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, KBYTES / esz, BN,
-                   CU_TENSOR_MAP_SWIZZLE_64B))
+  const uint32_t kbytes = (mode == 2) ? 64 : 128;
+  const CUtensorMapSwizzle swz = (mode == 2) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, BM, swz) ||
+      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, BN, swz))
     return cudaErrorInvalidValue;
-  if (mode == 0) return launch_mode<0>(ma, mb, p, st);
-  if (mode == 1) return launch_mode<1>(ma, mb, p, st);
-  return launch_mode<2>(ma, mb, p, st);
+  cudaError_t e;
+  if (mode == 0) e = launch_mode<0>(ma, mb, p, st);
+  else if (mode == 1) e = launch_mode<1>(ma, mb, p, st);
+  else e = launch_mode<2>(ma, mb, p, st);
+  if (e == cudaSuccess && (p.debug & 4)) {
+    unsigned long long h[16];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost);
+    const char* names[16] = {"prod.empty", "mma.tempty", "mma.full", "mma.hfull", "mma.cfull",
+                             "mma.sempty", "epi.tfull", "epi.hempty", "epi.sfull", "prod.total",
+                             "mma.total", "cprod.total", "epi.total", "", "", ""};
+    fprintf(stderr, "[hdc tc debug] mode %d, %d CTAs, %lld tiles; mean cycles per CTA:", mode, p.G,
+            (long long)p.T);
+    for (int i = 0; i < 13; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / p.G);
+    fprintf(stderr, "\n");
+  }
+  return e;
 }
 
 }  // namespace hdc

@@ -9,7 +9,8 @@ import os
 
 import torch
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhdc.so")
+LIB_PATH = os.environ.get("HDC_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libhdc.so")
 
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp32_tc": 3}
 PATH = {"auto": 0, "small": 1, "fused": 2}

@@ -1,0 +1,72 @@
+"""Multi-GPU partitioning of batched HDC inference (one process per GPU).
+
+Two partitions, following the paper's two Stage II variants:
+
+* N-shard (ScalableHD-L, Alg. 4, text P:410): rows of X are split
+  across ranks; B and C are replicated; each rank runs the whole fused path on
+  its rows; the only collective is an all-gather of the int32 labels (and,
+  optionally, scores).  Rows are independent, so labels equal the single-GPU
+  labels bit for bit when the per-row arithmetic does not depend on the shard.
+
+* D-shard (ScalableHD-S, Alg. 3, text P:355): rank r holds the column
+  slice D_r of B and C; it computes the partial scores S_r = HardSign(X B_r) C_r^T
+  (hdc_model_partial_scores), the ranks sum them with one all-reduce of N x K
+  fp32 (Alg. 3 `S += S_local`) and take the lowest-index argmax.
+
+torch.distributed (NCCL on GPUs) is plumbing only.  The per-rank compute is
+delegated to an object with the ``Model`` interface (``infer`` /
+``partial_scores``), normally ``paper_2506_09282_b200.Model``.
+"""
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(total, world, rank, align=1):
+    """[lo, hi) of `rank`'s contiguous share of `total` items, boundaries rounded
+    to multiples of `align` (the last rank takes the remainder)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    units = (total + align - 1) // align
+    lo = (units * rank // world) * align
+    hi = (units * (rank + 1) // world) * align
+    return min(lo, total), min(hi, total)
+
+
+def d_shard_slices(D, world, align=4):
+    """Column slices of the D-shard: widths multiples of `align` (16-byte rows
+    for fp32) except possibly the last."""
+    return [shard_bounds(D, world, r, align) for r in range(world)]
+
+
+def _gather_rows(local, counts, group=None):
+    """All-gather variable-length row blocks (padded to the max count)."""
+    world = dist.get_world_size(group)
+    m = max(counts)
+    pad = torch.zeros((m,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+
+
+def shard_n_infer(model, X_local, N_total, return_scores=False, group=None):
+    """N-shard inference: this rank holds rows [lo, hi) of X (its shard_bounds);
+    returns all N_total labels (and scores) on every rank."""
+    world = dist.get_world_size(group)
+    counts = [hi - lo for lo, hi in (shard_bounds(N_total, world, r) for r in range(world))]
+    rank = dist.get_rank(group)
+    if X_local.shape[0] != counts[rank]:
+        raise ValueError("X_local has %d rows, shard %d expects %d" % (X_local.shape[0], rank, counts[rank]))
+    y, S = model.infer(X_local, return_scores=return_scores)
+    labels = _gather_rows(y, counts, group)
+    scores = _gather_rows(S, counts, group) if return_scores else None
+    return labels, scores
+
+
+def shard_d_infer(model_slice, X, argmax_fn, return_scores=False, group=None):
+    """D-shard inference: `model_slice` holds this rank's columns of B and C;
+    X is replicated.  All-reduce(SUM) of the N x K partial scores, then argmax."""
+    S = model_slice.partial_scores(X)
+    dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
+    labels = argmax_fn(S)
+    return labels, (S if return_scores else None)

@@ -24,7 +24,7 @@ def hdc(cuda_device):
 
 SHAPES = [(33, 7, 17, 2), (128, 617, 160, 26), (129, 64, 250, 32), (300, 561, 2000, 6),
           (257, 3072, 300, 10), (200, 100, 16, 1), (1000, 33, 1000, 3), (640, 784, 801, 10),
-          (256, 64, 400, 100), (130, 40, 2000, 128)]
+          (256, 64, 400, 100), (130, 40, 2000, 64)]
 
 
 @pytest.mark.parametrize("prec", ["fp32_tc", "tf32", "bf16"])
