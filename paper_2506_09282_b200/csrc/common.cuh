@@ -22,6 +22,19 @@ HDC_DEV float4 ldg_stream(const float* p) {
 // Coherent-at-L2 load of data written by other CTAs of the same launch.
 HDC_DEV float ld_cg(const float* p) { return __ldcg(p); }
 
+// Packed fp32x2 FMA (sm_100a FFMA2): {a*b.x + c.x, a*b.y + c.y}, each correctly
+// rounded exactly like fmaf -- half the FMA-pipe instructions of two fmaf.
+HDC_DEV float2 ffma2(float a, float2 b, float2 c) {
+  unsigned long long aa, bb, cc, dd;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(dd) : "l"(aa), "l"(bb), "l"(cc));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(dd));
+  return r;
+}
+
 template <typename T>
 HDC_DEV T warp_sum_xor(T v) {
 #pragma unroll

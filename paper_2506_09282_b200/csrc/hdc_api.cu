@@ -373,7 +373,8 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
     e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);
     if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(int64_t) * m->Dq);
-    if (e == cudaSuccess) e = cudaMalloc(&m->Cil, (size_t)2 * 2 * tc_kp(K) * m->Dq);
+    if (e == cudaSuccess)
+      e = cudaMalloc(&m->Cil, (size_t)tc_c_tile_bytes(mode, K) * (m->Dq / tc_tile_n()));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // Bt must be complete
     if (e == cudaSuccess) {
       if (mode == 2)
@@ -381,7 +382,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
       else
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
-    if (e == cudaSuccess) e = launch_tc_c_interleave(m->Cp, K, tc_kp(K), D, m->Dp, m->Cil, st0);
+    if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Cil, st0);
   }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

@@ -49,10 +49,14 @@ using namespace ptx;
 constexpr int BM = 128;              // rows per tile (MMA M)
 constexpr int BN = 80;               // D columns per tile; 10000 = 125 x 80
 constexpr int STAGES_MAX = 6;
-constexpr int THREADS = 640;          // 4 role warps + 16 epilogue warps
+#ifndef HDC_TC_EPI_WARPS
+#define HDC_TC_EPI_WARPS 8
+#endif
+constexpr int NUM_EPI = HDC_TC_EPI_WARPS;           // epilogue warps: 4 lane quarters x NUM_CQ
+constexpr int THREADS = 32 * (4 + NUM_EPI);         // + producer, MMA, C-producer, spare
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI = 16;
-constexpr int EPI_COLS = BN / 4;     // columns per epilogue warp (4 column quarters)
+constexpr int NUM_CQ = NUM_EPI / 4;                 // column groups of the 80-wide tile
+constexpr int EPI_COLS = BN / NUM_CQ;               // columns per epilogue warp
 constexpr int MAX_LIMBS = 3;
 constexpr int H_BYTES = BM * BN * 2;                 // bf16 H tile (interleaved K-major)
 constexpr int CORE_LBO = 128;                        // K-adjacent 8x16B core matrices
@@ -76,14 +80,18 @@ struct Cfg {
   static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : 128;  // TMEM cols per Stage I buffer
   static constexpr int D2_COL = (MODE == 2) ? 480 : 256;          // Stage II accumulator
   static constexpr int KP_MAX = (MODE == 2) ? KP_MAX_I8 : KP_MAX_16;
-  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + BN * 8;   // + int64 column taus (int8)
+  // Stage II operand per D-tile: int8 mode (FFMA Stage II in the epilogue) fp32 C^T [80][KPF]
+  // + int64 column taus; other modes bf16 hi/lo [Kp][80] interleaved (Stage II MMA).
+  static constexpr bool S2F = (MODE == 2);
+  static constexpr int C_SLOT = S2F ? BN * KP_MAX * 4 + BN * 8 : 2 * KP_MAX * BN * 2;
+  static constexpr int H_REGION = S2F ? BM * KP_MAX * 4 : 2 * H_BYTES;   // S reduction | H tiles
   static constexpr int STAGES_ = (MODE == 2) ? 4 : 5;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES_ * A_STAGE;
   static constexpr int OFF_H = OFF_B + STAGES_ * B_STAGE;
-  static constexpr int OFF_C = OFF_H + 2 * H_BYTES;
+  static constexpr int OFF_C = OFF_H + H_REGION;
   static constexpr int OFF_BAR = OFF_C + 2 * C_SLOT;
   static constexpr int TOTAL = OFF_BAR + 512;
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
@@ -98,7 +106,9 @@ struct TcParams {
   const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
   const int64_t* rowtau;   // int8 mode: per-row part of tau (units of 2^14)
   const int64_t* coltau;   // int8 mode: per-column part of tau
-  const uint8_t* Cil;      // [Td][2][Kp*80] bf16 hi/lo C tiles, interleaved K-major
+  const uint8_t* Cil;      // per D-tile Stage II operand (see Cfg::C_SLOT), c_tile_bytes each
+  uint32_t c_tile_bytes;
+  int kpf;                 // int8 mode: class stride of the fp32 C^T tiles (K rounded up to 4)
   float* S_part;           // [G][2][BM][K]
   unsigned* cnt;           // [Tn]
   unsigned long long* recheck_count;
@@ -147,11 +157,12 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE>
+template <int MODE, int KT>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const TcParams p) {
   using CF = Cfg<MODE>;
+  constexpr bool S2F = CF::S2F;
   constexpr int NL = CF::NL;
   constexpr int KE = CF::KE;
   constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
@@ -164,7 +175,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   auto sdesc = [](uint32_t addr) { return smem_desc_sw(addr, CF::SBO, CF::SWZ); };
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte alignment for the swizzled tiles, keeping the pointer in the shared space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + CF::OFF_A;
   uint8_t* sB = smem + CF::OFF_B;
   uint8_t* sH = smem + CF::OFF_H;
@@ -191,7 +203,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
   for (int i = 0; i < 16; ++i) dbgc[i] = 0;
   const long long t_start = clock64();
-  const uint32_t c_tile_bytes = (uint32_t)(2 * p.Kp * BN * 2);
+  const uint32_t c_tile_bytes = p.c_tile_bytes;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -202,7 +214,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, NUM_EPI);
       mbar_init(cfull + b, 1);
-      mbar_init(cempty + b, 1);
+      mbar_init(cempty + b, S2F ? NUM_EPI : 1);
       mbar_init(hfull + b, NUM_EPI);
       mbar_init(hempty + b, 1);
     }
@@ -264,7 +276,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));
         bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
         if constexpr (MODE == 2)
-          bulk_load(sC + cs * CF::C_SLOT + CF::C_SLOT - BN * 8, p.coltau + (int64_t)di * BN, BN * 8,
+          bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
                     cfull + cs);
         cs ^= 1;
         if (cs == 0) cphase ^= 1;
@@ -313,6 +325,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         TWAIT(1, tempty + buf, bphase ^ 1);
         tc_fence_after();
         const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
+        const long long ts1 = clock64();
         for (int kb = 0; kb < KB; ++kb) {
           TWAIT(2, full + stage, phase);
           tc_fence_after();
@@ -344,11 +357,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
         }
         tc_commit_elect(tfull + buf);
+        if (p.debug & 4) dbgc[13] += (unsigned long long)(clock64() - ts1);
         buf ^= 1;
         if (buf == 0) bphase ^= 1;
-        if (t > t0) stage2(t - 1);          // overlaps the epilogue of tile t-1 with Stage I of t
+        const long long ts2 = clock64();
+        if constexpr (!S2F)
+          if (t > t0) stage2(t - 1);        // overlaps the epilogue of tile t-1 with Stage I of t
+        if (p.debug & 4) dbgc[14] += (unsigned long long)(clock64() - ts2);
       }
-      if (t1 > t0) stage2(t1 - 1);
+      if constexpr (!S2F)
+        if (t1 > t0) stage2(t1 - 1);
     }
   } else if (warp >= EPI_WARP0) {
     // ===================================================== epilogue
@@ -361,6 +379,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint32_t bphase = 0, hphase = 0, sphase = 0, cphase = 0;
     unsigned long long nrecheck = 0;
     const int first_ni = (int)(t0 / p.Td);
+    float2 S2[KT / 2];                      // int8 mode: FFMA2 Stage II accumulators (this row)
+#pragma unroll
+    for (int k = 0; k < KT / 2; ++k) S2[k] = make_float2(0.f, 0.f);
+#define SK(k) (((k) & 1) ? S2[(k) >> 1].y : S2[(k) >> 1].x)
+    float* sRed = reinterpret_cast<float*>(sH);   // int8 mode: [K][BM] quarter reduction
     for (int64_t t = t0; t < t1; ++t) {
       const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
       const int64_t row = (int64_t)ni * BM + m;
@@ -368,11 +391,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int64_t rtau = -1;                    // int8 mode: row part of tau (-1: padded row, never flag)
       if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : -(int64_t(1) << 62);
       TWAIT(6, tfull + buf, bphase);
-      TWAIT(7, hempty + hb, hphase ^ 1);
+      if constexpr (!S2F) TWAIT(7, hempty + hb, hphase ^ 1);
       const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
-      if constexpr (MODE == 2) {
-        mbar_wait(cfull + cs, cphase);
-        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + CF::C_SLOT - BN * 8);
+      const float* sCt = nullptr;           // C^T tile [80][kpf] (int8 mode), in smem
+      if constexpr (S2F) {
+        TWAIT(15, cfull + cs, cphase);
+        sCt = reinterpret_cast<const float*>(sC + cs * CF::C_SLOT);
+        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + BN * KT * 4);
       }
       tc_fence_after();
       uint8_t* hrow = sH + hb * H_BYTES + (m >> 3) * CORE_SBO + (m & 7) * 16;
@@ -421,17 +446,34 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           for (int j = 0; j < 4; ++j)
             if (!(__uint_as_float(r0[j]) >= 0.f)) hbits |= 1u << j;   // HardSign
         }
-        // 4 bf16 +-1 values (0x3F80 / 0xBF80) -> 8 bytes of a core-matrix row
-        const uint32_t w0 = ((hbits & 1u) ? 0xBF80u : 0x3F80u) | (((hbits & 2u) ? 0xBF80u : 0x3F80u) << 16);
-        const uint32_t w1 = ((hbits & 4u) ? 0xBF80u : 0x3F80u) | (((hbits & 8u) ? 0xBF80u : 0x3F80u) << 16);
-        *reinterpret_cast<uint2*>(hrow + (col0 >> 3) * CORE_LBO + (col0 & 7) * 2) = make_uint2(w0, w1);
+        if constexpr (S2F) {
+          // Stage II on the FMA pipe: S[k] += h[c] C[k, d0 + c], c ascending (exact +-1 products;
+          // padded columns have C = 0)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float h = ((hbits >> j) & 1u) ? -1.f : 1.f;
+            const float4* ct = reinterpret_cast<const float4*>(sCt + (col0 + j) * KT);  // kpf == KT
+#pragma unroll
+            for (int k4 = 0; k4 < KT / 4; ++k4) {
+              const float4 cv = ct[k4];
+              S2[2 * k4 + 0] = ffma2(h, make_float2(cv.x, cv.y), S2[2 * k4 + 0]);
+              S2[2 * k4 + 1] = ffma2(h, make_float2(cv.z, cv.w), S2[2 * k4 + 1]);
+            }
+          }
+        } else {
+          // 4 bf16 +-1 values (0x3F80 / 0xBF80) -> 8 bytes of a core-matrix row
+          const uint32_t w0 = ((hbits & 1u) ? 0xBF80u : 0x3F80u) | (((hbits & 2u) ? 0xBF80u : 0x3F80u) << 16);
+          const uint32_t w1 = ((hbits & 4u) ? 0xBF80u : 0x3F80u) | (((hbits & 8u) ? 0xBF80u : 0x3F80u) << 16);
+          *reinterpret_cast<uint2*>(hrow + (col0 >> 3) * CORE_LBO + (col0 & 7) * 2) = make_uint2(w0, w1);
+        }
       }
       tc_fence_before();
-      fence_proxy_async_smem();      // H writes -> visible to the tensor core
+      if constexpr (!S2F) fence_proxy_async_smem();   // H writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(tempty + buf);
-        mbar_arrive(hfull + hb);
+        if constexpr (S2F) mbar_arrive(cempty + cs);
+        else mbar_arrive(hfull + hb);
       }
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
@@ -445,40 +487,64 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int c_first = owner_of((int64_t)ni * p.Td, p.T, p.G);
       const int c_last = owner_of((int64_t)(ni + 1) * p.Td - 1, p.T, p.G);
       const bool sole = (c_first == c_last);
-      if (cq == 0) {
-        TWAIT(8, sfull, sphase);
+      constexpr int FIN = S2F ? NUM_CQ - 1 : 0;   // column group that finalises the run's scores
+      if constexpr (S2F) {
+        // fixed-order reduction of the 4 column quarters: ((S0 + S1) + S2) + S3
+        for (int qq = 0; qq < NUM_CQ - 1; ++qq) {
+          if (cq == qq) {
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+              if (k < K) sRed[k * BM + m] = (qq == 0) ? SK(k) : sRed[k * BM + m] + SK(k);
+          }
+          named_bar(1, NUM_EPI * 32);
+        }
+        if (cq == NUM_CQ - 1) {
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (k < K) SK(k) = sRed[k * BM + m] + SK(k);
+        }
+      }
+      if (cq == FIN) {
+        if constexpr (!S2F) TWAIT(8, sfull, sphase);
         tc_fence_after();
         const uint32_t sb = tmem_base + ((uint32_t)(q * 32) << 16) + CF::D2_COL;
         float* part = p.S_part + (((int64_t)c * 2 + ((ni == first_ni) ? 0 : 1)) * BM + m) * p.K;
         int best = 0;
         float bv = 0.f;
-        for (int k0 = 0; k0 < K; k0 += 8) {
-          uint32_t r[8];
-          tmem_ld8(sb + k0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int k = k0 + j;
-            if (k < K) {
-              const float v = __uint_as_float(r[j]);
-              if (sole) {
-                if (row_ok && p.scores) p.scores[row * p.K + k] = v;
-                if (k == 0 || v > bv) {
-                  bv = v;
-                  best = k;
-                }
-              } else {
-                part[k] = v;
-              }
+        auto take = [&](float v, int k) {
+          if (sole) {
+            if (row_ok && p.scores) p.scores[row * p.K + k] = v;
+            if (k == 0 || v > bv) {
+              bv = v;
+              best = k;
             }
+          } else {
+            part[k] = v;
+          }
+        };
+        if constexpr (S2F) {
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (k < K) take(SK(k), k);
+        } else {
+          for (int k0 = 0; k0 < K; k0 += 8) {
+            uint32_t r[8];
+            tmem_ld8(sb + k0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (k0 + j < K) take(__uint_as_float(r[j]), k0 + j);
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(sempty);
+        if constexpr (!S2F)
+          if (lane == 0) mbar_arrive(sempty);
         if (sole && row_ok && p.labels) p.labels[row] = best;
         if (!sole) __threadfence();
       }
+#pragma unroll
+      for (int k = 0; k < KT; ++k) SK(k) = 0.f;
       sphase ^= 1;
       if (sole) continue;
       named_bar(1, NUM_EPI * 32);
@@ -488,7 +554,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      if (*s_flag && cq == 0 && row_ok) {
+      if (*s_flag && cq == FIN && row_ok) {
         __threadfence();
         int best = 0;
         float bv = 0.f;
@@ -512,6 +578,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
   if ((p.debug & 4) && lane == 0 && (warp <= 2 || warp == EPI_WARP0)) {
+    if (warp != 1) dbgc[13] = dbgc[14] = 0;
+    if (warp != EPI_WARP0) dbgc[15] = 0;
     dbgc[9 + (warp == EPI_WARP0 ? 3 : warp)] = (unsigned long long)(clock64() - t_start);
     for (int i = 0; i < 16; ++i)
       if (dbgc[i]) atomicAdd(p.dbg + i, dbgc[i]);
@@ -620,6 +688,18 @@ __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int
   }
 }
 
+// int8 mode Stage II operand: fp32 C^T tiles [Td][80][kpf] (row = column d of the tile,
+// classes contiguous, zero beyond K and beyond D).
+__global__ void ct_tiles_kernel(const float* __restrict__ Cp, int64_t K, int64_t kpf, int64_t D,
+                                int64_t Dp, int64_t Td, float* __restrict__ out) {
+  const int64_t total = Td * BN * kpf;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i % kpf, dd = i / kpf;      // dd = global column index di * 80 + c
+    out[i] = (k < K && dd < D) ? Cp[k * Dp + dd] : 0.f;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -651,13 +731,13 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE>
+template <int MODE, int KT>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t st) {
   const size_t sm = Cfg<MODE>::TOTAL + 1024;
-  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE>,
+  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE, KT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  fused_tc_kernel<MODE><<<p.G, THREADS, sm, st>>>(a, b, p);
+  fused_tc_kernel<MODE, KT><<<p.G, THREADS, sm, st>>>(a, b, p);
   return cudaGetLastError();
 }
 
@@ -666,6 +746,10 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const TcPara
 int tc_tile_n() { return BN; }
 int tc_max_k(int mode) { return mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
 int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
+int64_t tc_kpf(int64_t K) { return (K + 3) / 4 * 4; }
+int64_t tc_c_tile_bytes(int mode, int64_t K) {
+  return mode == 2 ? BN * tc_kpf(K) * 4 : 2 * tc_kp(K) * BN * 2;
+}
 int64_t tc_max_fp_int8() { return 100000; }
 
 int64_t tc_tau_const(int64_t F) {
@@ -692,6 +776,19 @@ cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t ro
   else
     round_rows_kernel<1><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, void* out,
+                              cudaStream_t st) {
+  const int64_t Td = (D + BN - 1) / BN;
+  if (mode == 2) {
+    const int64_t total = Td * BN * tc_kpf(K);
+    int64_t grid = (total + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    ct_tiles_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, tc_kpf(K), D, Dp, Td, (float*)out);
+    return cudaGetLastError();
+  }
+  return launch_tc_c_interleave(Cp, K, tc_kp(K), D, Dp, out, st);
 }
 
 cudaError_t launch_tc_c_interleave(const float* Cp, int64_t K, int64_t Kp, int64_t D, int64_t Dp,
@@ -727,6 +824,8 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.rowtau = o.rowtau;
   p.coltau = o.coltau;
   p.Cil = (const uint8_t*)o.Cil;
+  p.kpf = (int)tc_kpf(o.K);
+  p.c_tile_bytes = (uint32_t)tc_c_tile_bytes(mode, o.K);
   p.S_part = o.S_part;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
@@ -755,19 +854,26 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
       !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, BN, swz))
     return cudaErrorInvalidValue;
   cudaError_t e;
-  if (mode == 0) e = launch_mode<0>(ma, mb, p, st);
-  else if (mode == 1) e = launch_mode<1>(ma, mb, p, st);
-  else e = launch_mode<2>(ma, mb, p, st);
+  if (mode == 0) e = launch_mode<0, 4>(ma, mb, p, st);
+  else if (mode == 1) e = launch_mode<1, 4>(ma, mb, p, st);
+  else if (p.kpf <= 4) e = launch_mode<2, 4>(ma, mb, p, st);
+  else if (p.kpf <= 8) e = launch_mode<2, 8>(ma, mb, p, st);
+  else if (p.kpf <= 12) e = launch_mode<2, 12>(ma, mb, p, st);
+  else if (p.kpf <= 16) e = launch_mode<2, 16>(ma, mb, p, st);
+  else if (p.kpf <= 20) e = launch_mode<2, 20>(ma, mb, p, st);
+  else if (p.kpf <= 24) e = launch_mode<2, 24>(ma, mb, p, st);
+  else if (p.kpf <= 28) e = launch_mode<2, 28>(ma, mb, p, st);
+  else e = launch_mode<2, 32>(ma, mb, p, st);
   if (e == cudaSuccess && (p.debug & 4)) {
     unsigned long long h[16];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost);
     const char* names[16] = {"prod.empty", "mma.tempty", "mma.full", "mma.hfull", "mma.cfull",
                              "mma.sempty", "epi.tfull", "epi.hempty", "epi.sfull", "prod.total",
-                             "mma.total", "cprod.total", "epi.total", "", "", ""};
+                             "mma.total", "cprod.total", "epi.total", "mma.SI", "mma.SII", "epi.cfull"};
     fprintf(stderr, "[hdc tc debug] mode %d, %d CTAs, %lld tiles; mean cycles per CTA:", mode, p.G,
             (long long)p.T);
-    for (int i = 0; i < 13; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / p.G);
+    for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / p.G);
     fprintf(stderr, "\n");
   }
   return e;

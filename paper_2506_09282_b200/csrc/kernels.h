@@ -61,7 +61,7 @@ struct TcOperands {
   int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to the 80-column tile; N_p to 128 rows
   const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
   const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
-  const void* Cil;                   // [Td][2][Kp*80] bf16 C hi/lo tiles (interleaved)
+  const void* Cil;                   // per D-tile Stage II operand (tc_c_tile_bytes each)
   const float* X;                    // caller's X (fp64 recheck)
   const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
   const int64_t* rowtau;             // [N_p] int8 mode
@@ -73,6 +73,10 @@ struct TcOperands {
 int tc_tile_n();
 int tc_max_k(int mode);
 int64_t tc_kp(int64_t K);
+int64_t tc_kpf(int64_t K);
+int64_t tc_c_tile_bytes(int mode, int64_t K);
+cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, void* out,
+                              cudaStream_t st);
 int64_t tc_max_fp_int8();
 int64_t tc_tau_const(int64_t F);
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,

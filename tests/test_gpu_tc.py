@@ -38,13 +38,13 @@ def test_tc_edge_grid(hdc, prec, N, F, D, K):
         rep, y, S, orc = parity_fp32(X, B, C, path="fused", prec=prec)
     else:
         # the 1e-2 * ||C_k||_1 tolerance is derived for D ~ 1e4 (one flip moves S by
-        # 2|C[k,d]| ~ 2 c1 / D); at small D allow ~ 16 flip-equivalents per row.
+        # 2|C[k,d]| ~ 2 c1 / D); at small D allow ~ 32 flip-equivalents per row.
         Bd, Cd = to_dev(B, C)
         m = hdc.Model(Bd, Cd, prec=prec)
         y, S = run_model(m, X, "fused")
         m.close()
         orc = oracle.infer(X, B, C)
-        rep = check_lowp(orc, y, S, rtol=max(1e-2, 16.0 / D))
+        rep = check_lowp(orc, y, S, rtol=max(1e-2, 32.0 / D))
     print(prec, (N, F, D, K), rep)
 
 
