@@ -44,11 +44,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--prec", default="fp32", choices=["fp32", "tf32", "bf16", "fp32_tc"])
+    ap.add_argument("--prec", default="fp32_tc", choices=["fp32", "tf32", "bf16", "fp32_tc"])
     ap.add_argument("--path", default="auto", choices=["auto", "small", "fused"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dshard", action="store_true",
+                    help="D-shard (small-N): each rank holds a column slice; all-reduce of N x K "
+                         "partial scores inside the timed step (strong scaling)")
     return ap.parse_args()
 
 
@@ -190,6 +193,7 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
                 "frac": achieved / peak, "traffic": None,
                 "algorithmic_per_launch": bytes_}
     achieved = flops / (ms_kernel * 1e-3) / 1e12
+    ceiling = None
     if prec == "fp32":
         mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak = N_SM * 128 * 2 * mhz * 1e6 / 1e12       # FFMA: 148 SM x 128 lanes x 2 flop
@@ -198,8 +202,15 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
         bf16 = float(peaks["bf16_tflops"])
         peak = bf16 / 2.0 if prec == "tf32" else bf16  # tf32 dense = 1/2 bf16 (nominal ratio)
         bound = "tensor"
-    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": flops}
+        if prec == "fp32_tc":
+            # sign-exact int8 limbs: 6 int8 MMAs per MAC = 3 bf16-MMA equivalents
+            ceiling = bf16 / 3.0
+    out = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+           "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": flops}
+    if ceiling:
+        out["path_ceiling"] = ceiling
+        out["frac_of_path_ceiling"] = achieved / ceiling
+    return out
 
 
 def run_ours(args, rank, world, local_rank):
@@ -213,20 +224,38 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg = CONFIGS[args.config]
     peaks, peaks_src = load_peaks()
-    B = torch.from_numpy(make_B(cfg)).to(dev)
-    C = torch.from_numpy(make_C(cfg)).to(dev)
-    # weak scaling: rank r infers rows [r N, (r+1) N) of the X stream
-    X = make_X_device(cfg, dev, rank * cfg.N, (rank + 1) * cfg.N)
+    Bh, Ch = make_B(cfg), make_C(cfg)
+    if args.dshard:
+        # D-shard: this rank's column slice of B and C; X replicated (rows 0..N)
+        from paper_2506_09282_b200.sharding import d_shard_slices
+        dlo, dhi = d_shard_slices(cfg.D, world)[rank]
+        Bh, Ch = Bh[:, dlo:dhi].copy(), Ch[:, dlo:dhi].copy()
+        X = make_X_device(cfg, dev, 0, cfg.N)
+    else:
+        # weak scaling: rank r infers rows [r N, (r+1) N) of the X stream
+        X = make_X_device(cfg, dev, rank * cfg.N, (rank + 1) * cfg.N)
+    B = torch.from_numpy(Bh).to(dev)
+    C = torch.from_numpy(Ch).to(dev)
     model = hdc.Model(B, C, prec=args.prec)
     labels = torch.empty(cfg.N, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    Sbuf = torch.empty(cfg.N, cfg.K, dtype=torch.float32, device=dev)
+
+    def step():
+        if args.dshard:
+            model.partial_scores(X, out=Sbuf)
+            if world > 1:
+                dist.all_reduce(Sbuf)
+            hdc.argmax(Sbuf, labels=labels)
+        else:
+            model.infer(X, labels=labels, path=args.path)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
 
     for _ in range(args.warmup):
-        model.infer(X, labels=labels, path=args.path)
+        step()
     torch.cuda.synchronize()
-    launches_per_step = model.last_launch_count()
+    launches_per_step = model.last_launch_count() + (1 if args.dshard else 0)
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -238,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
     for i in range(args.steps):
         flush.fill_(float(i))                          # evict X, B, C from L2 (untimed)
         starts[i].record(stream)
-        model.infer(X, labels=labels, path=args.path)
+        step()
         ends[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -251,11 +280,23 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = cfg.N * world * args.steps / (total_ms * 1e-3)
+    units = cfg.N if args.dshard else cfg.N * world
+    value = units * args.steps / (total_ms * 1e-3)
+
+    # dominant-kernel duration (library-recorded CUDA events on the launching
+    # stream, same flushed-L2 conditions) for the roofline; separate pass
+    model.set_kernel_timing(True)
+    kms = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        step()
+        kms.append(model.last_kernel_ms())
+    model.set_kernel_timing(False)
+    kernel_ms = sum(kms) / len(kms)
 
     # end to end through the public host-buffer entry point (H2D X, D2H labels)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.dshard:
         Xh = X.cpu().pin_memory()
         yh = torch.empty(cfg.N, dtype=torch.int32).pin_memory()
         for _ in range(2):
@@ -278,9 +319,10 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    roof = roofline_for(cfg, args.prec, args.path, ms_per_step / max(1, launches_per_step)
-                        if launches_per_step > 1 and cfg.N <= 32 else ms_per_step, peaks, clk["sm_mhz"])
+    roof = roofline_for(cfg, args.prec, args.path, kernel_ms, peaks, clk["sm_mhz"])
     roof["peak_source"] = peaks_src
+    roof["kernel_ms"] = kernel_ms
+    roof["kernel_share_of_step"] = kernel_ms / ms_per_step
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         rate, rows, dt, threads, _ = oracle_rate(cfg, args.cpu_seconds)
@@ -289,11 +331,12 @@ def run_ours(args, rank, world, local_rank):
                "cpu": cpu_model()}
     out = {"metric": "samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16", "fp32_tc": "bf16x3"}[args.prec],
+           "higher_is_better": True, "scaling": "strong" if args.dshard else "weak", "vs_baseline": None,
+           "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16", "fp32_tc": "i8x3"}[args.prec],
            "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
-                      "prec": args.prec, "path": args.path, "global_batch": cfg.N * world,
+                      "prec": args.prec, "path": args.path, "global_batch": units,
+                      "parallelism": ("dshard%d" % world) if args.dshard else ("dp%d" % world),
                       "l2": "flushed between steps (write of 2x L2 bytes, untimed)",
                       "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -56,9 +56,16 @@ typedef enum {
  *     (F+32) 2^-24 ||x_n|| ||b_d||, so each HardSign decision equals the one
  *     of the exact product X B (DESIGN.md §4 "sign recheck").
  *   HDC_PREC_TF32 / HDC_PREC_BF16: Stage I on tcgen05 tensor cores with X and B
- *     rounded to tf32 / bf16, fp32 accumulation; no recheck (approximate H).
- *   HDC_PREC_FP32_TC: Stage I on tcgen05 as 3 bf16 products (hi*hi + lo*hi +
- *     hi*lo) + the same float64 recheck, bound widened for the split error. */
+ *     rounded to tf32 (RNA) / bf16 (RN), fp32 accumulation; no recheck
+ *     (approximate H).  Stage II on tcgen05 with C split into bf16 hi + lo.
+ *   HDC_PREC_FP32_TC: sign-exact Stage I on the int8 tensor cores: each row of
+ *     X and column of B is scaled to a 21-bit integer image split into three
+ *     int8 limbs; the six limb products of weight >= 2^-14 accumulate EXACTLY
+ *     in int32 (tcgen05 kind::i8); every pre-activation within the rigorous
+ *     bound of that image is re-evaluated in float64 -> HardSign decisions
+ *     equal those of the exact product.  Stage II in fp32 FMA.
+ *     Falls back to the HDC_PREC_FP32 kernels (same guarantee) when K > 32 or
+ *     F > 100000.  Low-precision modes fall back likewise when K > 64. */
 typedef enum {
   HDC_PREC_FP32 = 0,
   HDC_PREC_TF32 = 1,
@@ -129,6 +136,13 @@ int64_t hdc_model_recheck_count(hdc_model_t m);
 
 /* Number of kernel launches the last call on this model enqueued. */
 int32_t hdc_model_last_launch_count(hdc_model_t m);
+
+/* Diagnostics for roofline reporting: when enabled, each call records CUDA
+ * events on its stream around its dominant kernel (the fused kernel, or the
+ * small-batch launches); hdc_model_last_kernel_ms synchronises on the last
+ * call's end event and returns the elapsed milliseconds (-1 if unavailable). */
+hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable);
+float hdc_model_last_kernel_ms(hdc_model_t m);
 
 const char* hdc_status_string(hdc_status_t st);
 /* Detail for the last failing call on this thread (thread-local, never NULL). */

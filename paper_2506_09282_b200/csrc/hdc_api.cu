@@ -80,6 +80,11 @@ struct hdc_model_s {
   int32_t* ldev = nullptr;
   float* sdev = nullptr;
   int32_t last_launches = 0;
+  // diagnostics: CUDA events around the dominant kernel of each call
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void tic(cudaStream_t st) { if (timing) cudaEventRecord(ev0, st); }
+  void toc(cudaStream_t st) { if (timing) cudaEventRecord(ev1, st); }
 
   ModelView view() const {
     ModelView v;
@@ -117,6 +122,8 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 }
 
 void free_model_memory(hdc_model_s* m) {
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
   cudaFree(m->Btc);
   cudaFree(m->coltau);
   cudaFree(m->Cil);
@@ -244,7 +251,9 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.S_part = m->S_part_tc;
   o.cnt = m->cnt_tc;
   o.recheck = m->recheck;
+  m->tic(st);
   e = launch_fused_tc(mode, o, N, scores, labels, m->num_sms, st);
+  m->toc(st);
   if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
   m->last_launches = 2;
   return HDC_OK;
@@ -266,7 +275,9 @@ hdc_status_t run_fused(hdc_model_s* m, const float* X, int64_t N, int32_t* label
   ws.recheck = m->recheck;
   cudaError_t e = launch_prep_x(X, N, m->F, m->Fp, m->Xt, m->xnorm, st);
   if (e != cudaSuccess) return cuda_fail(e, "prep_x launch");
+  m->tic(st);
   e = launch_fused_ffma(m->view(), ws, X, N, scores, labels, recheck, R, st);
+  m->toc(st);
   if (e != cudaSuccess) return cuda_fail(e, "fused_ffma launch");
   m->last_launches = 2;
   return HDC_OK;
@@ -283,6 +294,7 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   if (path == HDC_PATH_AUTO) path = (N <= kSmallMaxN) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
   if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
   const SmallWorkspace ws = m->small_ws();
+  m->tic(st);
   for (int64_t r0 = 0; r0 < N; r0 += kSmallMaxN) {
     const int n = (int)((N - r0) < kSmallMaxN ? (N - r0) : kSmallMaxN);
     cudaError_t e = launch_smallbatch(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
@@ -290,6 +302,7 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
     if (e != cudaSuccess) return cuda_fail(e, "smallbatch launch");
     ++m->last_launches;
   }
+  m->toc(st);
   return HDC_OK;
 }
 
@@ -503,5 +516,23 @@ int64_t hdc_model_recheck_count(hdc_model_t m) {
 }
 
 int32_t hdc_model_last_launch_count(hdc_model_t m) { return m ? m->last_launches : -1; }
+
+hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable) {
+  if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  if (enable && !m->ev0) {
+    if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess)
+      return fail(HDC_ERR_CUDA, "event creation");
+  }
+  m->timing = enable != 0;
+  return HDC_OK;
+}
+
+float hdc_model_last_kernel_ms(hdc_model_t m) {
+  if (!m || !m->timing || !m->ev0) return -1.f;
+  if (cudaEventSynchronize(m->ev1) != cudaSuccess) return -1.f;
+  float ms = -1.f;
+  if (cudaEventElapsedTime(&ms, m->ev0, m->ev1) != cudaSuccess) return -1.f;
+  return ms;
+}
 
 }  // extern "C"

@@ -47,6 +47,10 @@ def lib():
         L.hdc_model_recheck_count.restype = I64
         L.hdc_model_last_launch_count.argtypes = [P]
         L.hdc_model_last_launch_count.restype = ctypes.c_int32
+        L.hdc_model_set_kernel_timing.argtypes = [P, I32]
+        L.hdc_model_set_kernel_timing.restype = I32
+        L.hdc_model_last_kernel_ms.argtypes = [P]
+        L.hdc_model_last_kernel_ms.restype = ctypes.c_float
         L.hdc_status_string.argtypes = [I32]
         L.hdc_status_string.restype = ctypes.c_char_p
         L.hdc_last_error.restype = ctypes.c_char_p
@@ -138,6 +142,12 @@ class Model:
 
     def last_launch_count(self):
         return int(lib().hdc_model_last_launch_count(self._h))
+
+    def set_kernel_timing(self, enable=True):
+        _check(lib().hdc_model_set_kernel_timing(self._h, 1 if enable else 0))
+
+    def last_kernel_ms(self):
+        return float(lib().hdc_model_last_kernel_ms(self._h))
 
     def close(self):
         if self._h:
