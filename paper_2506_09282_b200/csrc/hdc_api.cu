@@ -49,6 +49,7 @@ struct hdc_model_s {
   hdc_precision_t prec = HDC_PREC_FP32;
   float* Bp = nullptr;
   float* Bt = nullptr;
+  float* B4 = nullptr;       // unit-major copy of Bp for the small-batch kernel
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
   int64_t Dq = 0;            // D rounded up to the tensor-core D tile (80)
   void* Btc = nullptr;       // [NL][Dq][Fp]
@@ -64,8 +65,7 @@ struct hdc_model_s {
   float* bnorm = nullptr;
   // small-batch workspace
   float* S_part = nullptr;
-  float* S_grp = nullptr;
-  unsigned* cnt = nullptr;  // [G1 + 1]
+  unsigned* cnt = nullptr;  // [4] last-arriver counter of K2
   unsigned long long* recheck = nullptr;
   // fused-path workspace, grown on demand with N
   int64_t fw_rows = 0;  // Np capacity
@@ -95,6 +95,7 @@ struct hdc_model_s {
     v.Fp = Fp;
     v.Bp = Bp;
     v.Bt = Bt;
+    v.B4 = B4;
     v.Cp = Cp;
     v.bnorm = bnorm;
     v.tau_coef = sign_bound_coef(F);
@@ -103,9 +104,7 @@ struct hdc_model_s {
   SmallWorkspace small_ws() const {
     SmallWorkspace w;
     w.S_part = S_part;
-    w.S_grp = S_grp;
     w.cnt1 = cnt;
-    w.cnt2 = cnt + small_num_groups(D);
     w.recheck = recheck;
     return w;
   }
@@ -133,6 +132,7 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->cnt_tc);
   cudaFree(m->Bp);
   cudaFree(m->Bt);
+  cudaFree(m->B4);
   cudaFree(m->Xt);
   cudaFree(m->xnorm);
   cudaFree(m->S_part_f);
@@ -140,7 +140,6 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Cp);
   cudaFree(m->bnorm);
   cudaFree(m->S_part);
-  cudaFree(m->S_grp);
   cudaFree(m->cnt);
   cudaFree(m->recheck);
   cudaFree(m->Xdev);
@@ -294,11 +293,13 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   if (path == HDC_PATH_AUTO) path = (N <= kSmallMaxN) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
   if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
   const SmallWorkspace ws = m->small_ws();
+  const int chunk = small_max_rows(m->F, m->D, m->K, m->num_sms);
+  if (chunk < 1) return fail(HDC_ERR_UNSUPPORTED, "F too large for the small-batch kernel's shared memory");
   m->tic(st);
-  for (int64_t r0 = 0; r0 < N; r0 += kSmallMaxN) {
-    const int n = (int)((N - r0) < kSmallMaxN ? (N - r0) : kSmallMaxN);
+  for (int64_t r0 = 0; r0 < N; r0 += chunk) {
+    const int n = (int)((N - r0) < chunk ? (N - r0) : chunk);
     cudaError_t e = launch_smallbatch(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
-                                      labels ? labels + r0 : nullptr, recheck, st);
+                                      labels ? labels + r0 : nullptr, recheck, m->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "smallbatch launch");
     ++m->last_launches;
   }
@@ -354,17 +355,17 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   m->Fp = round_up(F, kFPad);
   cudaGetDevice(&m->device);
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
-  const int64_t G = small_num_tiles(D), G1 = small_num_groups(D);
+  const int64_t G = 1024;  // >= small_num_ctas for any device
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, bytes)                                           \
   if (e == cudaSuccess) e = cudaMalloc((void**)&(ptr), (size_t)(bytes));
   ALLOC(m->Bp, sizeof(float) * m->Fp * m->Dp);
   ALLOC(m->Bt, sizeof(float) * m->Fp * m->Dp);
+  ALLOC(m->B4, sizeof(float) * m->Fp * m->Dp);
   ALLOC(m->Cp, sizeof(float) * K * m->Dp);
   ALLOC(m->bnorm, sizeof(float) * m->Dp);
   ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
-  ALLOC(m->S_grp, sizeof(float) * G1 * kSmallMaxN * K);
-  ALLOC(m->cnt, sizeof(unsigned) * (G1 + 1));
+  ALLOC(m->cnt, sizeof(unsigned) * 4);
   ALLOC(m->recheck, sizeof(unsigned long long));
 #undef ALLOC
   if (e != cudaSuccess) {
@@ -378,9 +379,10 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = cudaMemset(m->Bp, 0, sizeof(float) * m->Fp * m->Dp);
   if (e == cudaSuccess) e = launch_pad_copy(B, F, D, m->Bp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_transpose(m->Bp, m->Fp, m->Dp, m->Bt, st0);
+  if (e == cudaSuccess) e = launch_unit_major(m->Bp, m->Fp, m->Dp, m->B4, st0);
   if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
-  if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * (G1 + 1));
+  if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 4);
   m->Dq = (D + tc_tile_n() - 1) / tc_tile_n() * tc_tile_n();
   const int mode = tc_mode_of(m);
   if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {

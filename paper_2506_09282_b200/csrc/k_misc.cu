@@ -56,6 +56,17 @@ __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, in
   }
 }
 
+// B4[u][f][j] = Bp[f][4u + j]: all rows of a 4-column unit contiguous.
+__global__ void unit_major_kernel(const float4* __restrict__ Bp, int64_t Fp, int64_t U,
+                                  float4* __restrict__ B4) {
+  const int64_t total = Fp * U;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = i / Fp, f = i % Fp;
+    B4[i] = Bp[f * U + u];
+  }
+}
+
 // ||b_d||_2 in float64, rounded UP to fp32 (it only feeds an upper bound).
 __global__ void col_norm_kernel(const float* __restrict__ Bp, int64_t F, int64_t Dp, int64_t D,
                                 float* __restrict__ out) {
@@ -93,6 +104,15 @@ cudaError_t launch_transpose(const float* src, int64_t rows, int64_t cols, float
                              cudaStream_t st) {
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unit_major(const float* Bp, int64_t Fp, int64_t Dp, float* B4, cudaStream_t st) {
+  const int64_t total = Fp * (Dp / 4);
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  unit_major_kernel<<<(unsigned)grid, 256, 0, st>>>(reinterpret_cast<const float4*>(Bp), Fp, Dp / 4,
+                                                    reinterpret_cast<float4*>(B4));
   return cudaGetLastError();
 }
 

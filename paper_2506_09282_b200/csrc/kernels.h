@@ -13,6 +13,7 @@ struct ModelView {
   int64_t Dp;            // D padded to a multiple of kDPad (zero columns)
   const float* Bp;       // Fp x Dp fp32, zero-padded rows and columns
   const float* Bt;       // Dp x Fp fp32: B transposed (fp64 sign recheck gathers)
+  const float* B4;       // unit-major copy [Dp/4][Fp][4] (small-batch streaming)
   const float* Cp;       // K x Dp fp32, zero-padded columns
   const float* bnorm;    // Dp: ||b_d||_2 rounded up (0 on padding)
   float tau_coef;        // sign_bound_coef(F)
@@ -23,20 +24,18 @@ constexpr int64_t kFPad = 64;   // F padding granule (covers every kernel's K st
 
 // Workspace for the small-batch kernel's cross-CTA reduction.
 struct SmallWorkspace {
-  float* S_part;         // [G][32][K]
-  float* S_grp;          // [G1][32][K]
-  unsigned* cnt1;        // [G1], zero between launches
-  unsigned* cnt2;        // [1],  zero between launches
+  float* S_part;         // [num_sms][32][K]
+  unsigned* cnt1;        // [1], zero between launches
   unsigned long long* recheck;  // fp64 re-evaluation counter (diagnostic)
 };
 
-int64_t small_num_tiles(int64_t Dp);     // G
-int64_t small_num_groups(int64_t Dp);    // G1
+int64_t small_num_ctas(int64_t D, int num_sms);                       // CTAs of K2
+int small_max_rows(int64_t F, int64_t D, int64_t K, int num_sms);     // rows per K2 launch
 
-// K2: rows [0, n) of X (n <= 32), all of D.  Writes S (n x K) to `scores` when
-// non-null and argmax labels to `labels` when non-null.
+// K2: rows [0, n) of X (n <= small_max_rows), all of D.  Writes S (n x K) to
+// `scores` when non-null and argmax labels to `labels` when non-null.
 cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, const float* X,
-                              int n, float* scores, int32_t* labels, bool recheck,
+                              int n, float* scores, int32_t* labels, bool recheck, int num_sms,
                               cudaStream_t st);
 
 // Workspace of the fused large-batch kernels (grown with N).
@@ -97,6 +96,7 @@ cudaError_t launch_pad_copy(const float* src, int64_t rows, int64_t cols, float*
                             int64_t dst_cols, cudaStream_t st);
 cudaError_t launch_transpose(const float* src, int64_t rows, int64_t cols, float* dst,
                              cudaStream_t st);  // dst[c][r] = src[r][c]
+cudaError_t launch_unit_major(const float* Bp, int64_t Fp, int64_t Dp, float* B4, cudaStream_t st);
 cudaError_t launch_col_norms(const float* Bp, int64_t F, int64_t Dp, int64_t D, float* out,
                              cudaStream_t st);
 
