@@ -12,8 +12,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "lib", "libhdc.so")
+# HDC_BUILD_TAG / HDC_NVCC_DEFS: side builds for A/B measurements (lib/libhdc_<tag>.so,
+# loaded through HDC_LIB_PATH); the default build is the product.
+_TAG = os.environ.get("HDC_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(PKG, "lib", "libhdc%s.so" % ("_" + _TAG if _TAG else ""))
+DEFS = os.environ.get("HDC_NVCC_DEFS", "").split() if _TAG else []
 GEN_SRC = os.path.join(ROOT, "hdc_inputs", "csrc", "hdcgen.cu")
 GEN_LIB = os.path.join(ROOT, "hdc_inputs", "libhdcgen.so")
 
@@ -51,7 +55,7 @@ def build(force=False, verbose=False, ptxas_info=False):
         o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC] + ARCH + FLAGS + extra + ["-c", s, "-o", o])
+            jobs.append([NVCC] + ARCH + FLAGS + DEFS + extra + ["-c", s, "-o", o])
     outs = []
     if jobs:
         with concurrent.futures.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
@@ -60,7 +64,7 @@ def build(force=False, verbose=False, ptxas_info=False):
         tmp = LIB + ".tmp%d" % os.getpid()
         _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcuda"])
         os.replace(tmp, LIB)
-    if force or _stale(GEN_LIB, [GEN_SRC]):
+    if not _TAG and (force or _stale(GEN_LIB, [GEN_SRC])):
         tmp = GEN_LIB + ".tmp%d" % os.getpid()
         _run([NVCC] + ARCH + FLAGS + ["-shared", GEN_SRC, "-o", tmp])
         os.replace(tmp, GEN_LIB)

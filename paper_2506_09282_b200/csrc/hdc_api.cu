@@ -51,12 +51,14 @@ struct hdc_model_s {
   float* Bt = nullptr;
   float* B4 = nullptr;       // unit-major copy of Bp for the small-batch kernel
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
-  int64_t Dq = 0;            // D rounded up to the tensor-core D tile (80)
+  int64_t Dq = 0;            // D rounded up to cl_d tensor-core D tiles (tc_tile_n)
+  int cl_n = 1, cl_d = 1;    // K4 thread-block cluster (multicast) shape
   void* Btc = nullptr;       // [NL][Dq][Fp]
   int64_t* coltau = nullptr; // [Dq] (int8 limbs)
-  void* Cil = nullptr;       // [Td][2][Kp*80] bf16 hi/lo C tiles for the Stage II MMA
+  void* Cil = nullptr;       // per D-tile Stage II operand (tc_c_tile_bytes each)
   // tensor-core workspace, grown with N
   int64_t tw_rows = 0;
+  int64_t tw_slots = 0;      // capacity of S_part_tc in [128][K] slots
   void* Atc = nullptr;       // [NL][Np][Fp]
   int64_t* rowtau = nullptr; // [Np]
   float* S_part_tc = nullptr;
@@ -197,8 +199,13 @@ bool tc_eligible(const hdc_model_s* m) {
 
 hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   const int mode = tc_mode_of(m);
-  const int64_t Np = (N + kTileM - 1) / kTileM * kTileM;
-  if (Np <= m->tw_rows) return HDC_OK;
+  const int64_t gm = kTileM * m->cl_n;
+  const int64_t Np = (N + gm - 1) / gm * gm;
+  const int64_t slots = tc_s_part_slots(Np / kTileM, m->Dq / tc_tile_n(mode, m->K), m->cl_n, m->cl_d,
+                                        m->num_sms);
+  if (Np <= m->tw_rows && slots <= m->tw_slots) return HDC_OK;
+  const int64_t rows = Np > m->tw_rows ? Np : m->tw_rows;
+  const int64_t nsl = slots > m->tw_slots ? slots : m->tw_slots;
   cudaDeviceSynchronize();
   cudaFree(m->Atc);
   cudaFree(m->rowtau);
@@ -206,17 +213,18 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   cudaFree(m->cnt_tc);
   m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->cnt_tc = nullptr;
   m->tw_rows = 0;
-  cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * Np * m->Fp);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(int64_t) * Np);
-  if (e == cudaSuccess)
-    e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * m->num_sms * 2 * kTileM * m->K);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (Np / kTileM));
-  if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (Np / kTileM));
+  m->tw_slots = 0;
+  cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * rows * m->Fp);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(int64_t) * rows);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * nsl * kTileM * m->K);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (rows / kTileM));
+  if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (rows / kTileM));
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(HDC_ERR_NO_MEMORY, "tensor-core workspace allocation");
   }
-  m->tw_rows = Np;
+  m->tw_rows = rows;
+  m->tw_slots = nsl;
   return HDC_OK;
 }
 
@@ -225,7 +233,8 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   const int mode = tc_mode_of(m);
   hdc_status_t stt = ensure_tc_ws(m, N);
   if (stt != HDC_OK) return stt;
-  const int64_t Np = (N + kTileM - 1) / kTileM * kTileM;
+  const int64_t gm = kTileM * m->cl_n;
+  const int64_t Np = (N + gm - 1) / gm * gm;
   cudaError_t e;
   if (mode == 2)
     e = launch_tc_limbs(X, N, Np, m->F, m->F, m->Fp, (int8_t*)m->Atc, m->rowtau, tc_tau_const(m->F), st);
@@ -240,6 +249,8 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.Dq = m->Dq;
   o.K = m->K;
   o.N_p = Np;
+  o.cl_n = m->cl_n;
+  o.cl_d = m->cl_d;
   o.A = m->Atc;
   o.B = m->Btc;
   o.Cil = m->Cil;
@@ -248,6 +259,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.rowtau = m->rowtau;
   o.coltau = m->coltau;
   o.S_part = m->S_part_tc;
+  o.s_part_slots = m->tw_slots;
   o.cnt = m->cnt_tc;
   o.recheck = m->recheck;
   m->tic(st);
@@ -383,13 +395,15 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 4);
-  m->Dq = (D + tc_tile_n() - 1) / tc_tile_n() * tc_tile_n();
   const int mode = tc_mode_of(m);
+  const int64_t tn = tc_tile_n(mode < 0 ? 0 : mode, K);
+  tc_cluster_shape(mode < 0 ? 0 : mode, K, &m->cl_n, &m->cl_d);
+  m->Dq = (D + tn * m->cl_d - 1) / (tn * m->cl_d) * (tn * m->cl_d);
   if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
     e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);
     if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(int64_t) * m->Dq);
     if (e == cudaSuccess)
-      e = cudaMalloc(&m->Cil, (size_t)tc_c_tile_bytes(mode, K) * (m->Dq / tc_tile_n()));
+      e = cudaMalloc(&m->Cil, (size_t)tc_c_tile_bytes(mode, K) * (m->Dq / tn));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // Bt must be complete
     if (e == cudaSuccess) {
       if (mode == 2)
@@ -397,7 +411,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
       else
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
-    if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Cil, st0);
+    if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Dq, m->Cil, st0);
   }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

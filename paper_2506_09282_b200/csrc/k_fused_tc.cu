@@ -47,7 +47,6 @@ namespace {
 using namespace ptx;
 
 constexpr int BM = 128;              // rows per tile (MMA M)
-constexpr int BN = 80;               // D columns per tile; 10000 = 125 x 80
 constexpr int STAGES_MAX = 6;
 #ifndef HDC_TC_EPI_WARPS
 #define HDC_TC_EPI_WARPS 8
@@ -55,18 +54,22 @@ constexpr int STAGES_MAX = 6;
 constexpr int NUM_EPI = HDC_TC_EPI_WARPS;           // epilogue warps: 4 lane quarters x NUM_CQ
 constexpr int THREADS = 32 * (4 + NUM_EPI);         // + producer, MMA, C-producer, spare
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_CQ = NUM_EPI / 4;                 // column groups of the 80-wide tile
-constexpr int EPI_COLS = BN / NUM_CQ;               // columns per epilogue warp
+constexpr int NUM_CQ = NUM_EPI / 4;                 // column groups of the tile
 constexpr int MAX_LIMBS = 3;
-constexpr int H_BYTES = BM * BN * 2;                 // bf16 H tile (interleaved K-major)
 constexpr int CORE_LBO = 128;                        // K-adjacent 8x16B core matrices
-constexpr int CORE_SBO = (BN / 8) * 128;             // 8-row groups (10 core matrices)
 constexpr int KP_MAX_I8 = 32;                        // Stage II N (classes) limits
 constexpr int KP_MAX_16 = 64;
-constexpr int C_SLOT_MAX = 2 * KP_MAX_16 * BN * 2;   // bf16 hi + lo, [Kp][80] each
 
-template <int MODE>
+// D-tile width by mode and class count: 160 for bf16/tf32 with K <= 32 (an N=160
+// MMA costs the same cycles as N=80, tools/mma_microbench.cu), else 80
+// (int8: three limb accumulators x 80 columns x 2 buffers fill TMEM).
+__host__ __device__ constexpr int tile_n_for(int mode, int64_t K) {
+  return (mode == 2) ? 80 : (K <= 32 ? 160 : 80);
+}
+
+template <int MODE, int BN_>
 struct Cfg {
+  static constexpr int BN = BN_;
   static constexpr int NL = (MODE == 2) ? 3 : 1;
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
   // K bytes per stage = one swizzle-atom row: 128 B (SWIZZLE_128B) for the single-operand
@@ -76,40 +79,59 @@ struct Cfg {
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
   static constexpr int A_LIMB_BYTES = BM * KBYTES;
   static constexpr int B_LIMB_BYTES = BN * KBYTES;
-  static constexpr int KE = KBYTES / ESZ;                      // K elements per stage
-  static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : 128;  // TMEM cols per Stage I buffer
-  static constexpr int D2_COL = (MODE == 2) ? 480 : 256;          // Stage II accumulator
-  static constexpr int KP_MAX = (MODE == 2) ? KP_MAX_I8 : KP_MAX_16;
-  // Stage II operand per D-tile: int8 mode (FFMA Stage II in the epilogue) fp32 C^T [80][KPF]
-  // + int64 column taus; other modes bf16 hi/lo [Kp][80] interleaved (Stage II MMA).
-  static constexpr bool S2F = (MODE == 2);
-  static constexpr int C_SLOT = S2F ? BN * KP_MAX * 4 + BN * 8 : 2 * KP_MAX * BN * 2;
-  static constexpr int H_REGION = S2F ? BM * KP_MAX * 4 : 2 * H_BYTES;   // S reduction | H tiles
-  static constexpr int STAGES_ = (MODE == 2) ? 4 : 5;
+  static constexpr int KE = KBYTES / ESZ;                        // K elements per stage
+  static constexpr int KP_MAX = (MODE == 2 || BN > 80) ? KP_MAX_I8 : KP_MAX_16;
+  // TMEM columns: two Stage I accumulator buffers, the Stage II accumulator (hi and lo C
+  // parts accumulate into the same Kp columns) and, for bf16/tf32, two H tiles as the
+  // Stage II A operand (bf16 pairs, BN/2 columns each).
+  static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : (BN <= 128 ? 128 : BN);
+  static constexpr int D2_COL = 2 * ACC_STRIDE;
+  static constexpr bool H_TMEM = (MODE != 2);
+  static constexpr int S_COLS = KP_MAX;
+  static constexpr int H_COL = D2_COL + S_COLS;
+  static constexpr int NH = 2;                                    // H tile buffers
+  static_assert(H_COL + (H_TMEM ? NH * BN / 2 : 0) <= 512, "TMEM budget");
+  static constexpr int H_BYTES = BM * BN * 2;                    // int8 mode: bf16 H tile in smem
+  static constexpr int CORE_SBO = (BN / 8) * 128;                // 8-row groups of core matrices
+  static constexpr int EPI_COLS = BN / NUM_CQ;                   // columns per epilogue thread
+  static constexpr int CH = (EPI_COLS % 16 == 0) ? 16 : 8;       // columns per TMEM load
+  static constexpr int NWB = (EPI_COLS + 31) / 32;               // bit words per thread
+  // Stage II operand per D-tile: bf16 hi/lo [2][Kp][BN] interleaved; int8 mode appends the
+  // int64 column taus of the tile.
+  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + (MODE == 2 ? BN * 8 : 0);
+  static constexpr int H_REGION = H_TMEM ? 0 : NH * H_BYTES;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
+  static constexpr int FIXED = H_REGION + 2 * C_SLOT + 512 + 1024 + 16;
+  static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / (A_STAGE + B_STAGE);
+  static constexpr int STAGES_ = STAGES_FIT < STAGES_MAX ? STAGES_FIT : STAGES_MAX;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES_ * A_STAGE;
   static constexpr int OFF_H = OFF_B + STAGES_ * B_STAGE;
   static constexpr int OFF_C = OFF_H + H_REGION;
-  static constexpr int OFF_BAR = OFF_C + 2 * C_SLOT;
+  static constexpr int OFF_BAR = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;
   static constexpr int TOTAL = OFF_BAR + 512;
+  static_assert(STAGES_ >= 3, "pipeline depth");
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
+  static_assert(C_SLOT % 16 == 0, "bulk-copy granule");
   static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
 };
 
 struct TcParams {
   int64_t N, F, Fp, D, Dp, Dq, K, Kp, Np;
-  int Tn, Td, G;
-  int64_t T;
+  int Tn, Td, G;            // G = clusters of the launch
+  int TdG;                  // D-groups: a cluster tile = CLN N-tiles x CLD consecutive D-tiles
+  int64_t T;                // cluster tiles (n-major), contiguous ranges per cluster
   const float* X;          // caller's X (fp64 recheck)
   const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
   const int64_t* rowtau;   // int8 mode: per-row part of tau (units of 2^14)
   const int64_t* coltau;   // int8 mode: per-column part of tau
   const uint8_t* Cil;      // per D-tile Stage II operand (see Cfg::C_SLOT), c_tile_bytes each
   uint32_t c_tile_bytes;
-  int kpf;                 // int8 mode: class stride of the fp32 C^T tiles (K rounded up to 4)
-  float* S_part;           // [G][2][BM][K]
+  float* S_part;           // [CTAs][nslot][BM][K] partial scores of split N-tiles
+  int64_t s_part_cap;      // capacity of S_part in [BM][K] slots
+  int nslot;               // slots per CTA: 2 (CLD = 1: first / last N-group of the range),
+                           // else one per N-group of the cluster's range
   unsigned* cnt;           // [Tn]
   unsigned long long* recheck_count;
   float* scores;
@@ -148,7 +170,18 @@ __device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, in
   const float* xr = p.X + row * p.F;
   const float* br = p.Bt + d * p.Fp;
   double s = 0.0;
-  for (int64_t f = lane; f < p.F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
+  int64_t f = lane;
+  for (; f + 96 < p.F; f += 128) {       // 8 independent loads in flight, then the FMAs in f order
+    float xv[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = __ldg(xr + f + 32 * u);
+      bv[u] = __ldg(br + f + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = fma((double)xv[u], (double)bv[u], s);
+  }
+  for (; f < p.F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
   s = warp_sum_xor(s);
   return s >= 0.0 ? 1.f : -1.f;
 }
@@ -157,14 +190,18 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE, int KT>
+template <int MODE, int BN, int CLN, int CLD>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const TcParams p) {
-  using CF = Cfg<MODE>;
-  constexpr bool S2F = CF::S2F;
+  using CF = Cfg<MODE, BN>;
   constexpr int NL = CF::NL;
   constexpr int KE = CF::KE;
+  constexpr int NH = CF::NH;
+  constexpr int EPI_COLS = CF::EPI_COLS;
+  constexpr int CH = CF::CH;
+  constexpr int NWB = CF::NWB;
+  constexpr int CORE_SBO = CF::CORE_SBO;
   constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
   constexpr uint32_t IDESC_N160 = make_idesc<MODE>(BM, 2 * BN);
   constexpr uint32_t IDESC_N240 = make_idesc<MODE>(BM, 3 * BN);
@@ -185,19 +222,31 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint64_t* full = bars;                 // [STAGES] operands landed
   uint64_t* empty = bars + STAGES;       // [STAGES] operands consumed
   uint64_t* tfull = bars + 2 * STAGES;   // [2] Stage I accumulator ready
-  uint64_t* tempty = tfull + 2;          // [2] Stage I accumulator drained
-  uint64_t* cfull = tempty + 2;          // [2] C tile landed
+  uint64_t* tempty = tfull + 2;          // [2] Stage I accumulator drained (read into registers)
+  uint64_t* cfull = tempty + 2;          // [2] C tile (+ column taus) landed
   uint64_t* cempty = cfull + 2;          // [2] C tile consumed (Stage II MMA done)
-  uint64_t* hfull = cempty + 2;          // [2] H tile written
-  uint64_t* hempty = hfull + 2;          // [2] H tile consumed
+  uint64_t* hfull = cempty + 2;          // [NH] H tile written
+  uint64_t* hempty = hfull + 2;          // [NH] H tile consumed
   uint64_t* sfull = hempty + 2;          // [1] Stage II accumulator of a run complete
   uint64_t* sempty = sfull + 1;          // [1] Stage II accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 1);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
+  // Cluster of CLN x CLD CTAs: rank (rn, rd) works on N-tile ng CLN + rn and D-tile
+  // dg CLD + rd of cluster tile (ng, dg).  The CLD CTAs sharing an N-tile multicast
+  // its X tile (each loads 128/CLD rows), the CLN CTAs sharing a D-tile multicast its
+  // B tile (BN/CLN rows each): L2 -> SM traffic per tile falls by those factors.
+  constexpr int CLS = CLN * CLD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const int64_t t0 = range_begin(c, p.T, p.G), t1 = range_begin(c + 1, p.T, p.G);
+  const int c = blockIdx.x;                        // global CTA index (partial-score slots)
+  const int rank = (CLS > 1) ? (int)cluster_ctarank() : 0;
+  const int rn = rank / CLD, rd = rank % CLD;
+  const int cl = c / CLS;                          // cluster index
+  const uint16_t a_mask = (uint16_t)(((1u << CLD) - 1u) << (rn * CLD));   // same N-tile
+  uint16_t b_mask = 0;                                                    // same D-tile
+#pragma unroll
+  for (int i = 0; i < CLN; ++i) b_mask |= (uint16_t)(1u << (i * CLD + rd));
+  const int64_t t0 = range_begin(cl, p.T, p.G), t1 = range_begin(cl + 1, p.T, p.G);
   const int KB = (int)(p.Fp / KE);
   unsigned long long dbgc[16];
 #pragma unroll
@@ -208,18 +257,18 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CLN + CLD - 1);   // MMA commits of every CTA this one multicasts to
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, NUM_EPI);
       mbar_init(cfull + b, 1);
-      mbar_init(cempty + b, S2F ? NUM_EPI : 1);
+      mbar_init(cempty + b, 1);
       mbar_init(hfull + b, NUM_EPI);
       mbar_init(hempty + b, 1);
     }
     mbar_init(sfull, 1);
-    mbar_init(sempty, 4);               // the 4 warps of column quarter 0 drain S
+    mbar_init(sempty, 4);               // the 4 warps of column group 0 drain S
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -228,7 +277,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CLS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -237,25 +287,26 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      constexpr int AR = BM / CLD, BR = BN / CLN;    // rows of the A / B tile this CTA loads
       for (int64_t t = t0; t < t1; ++t) {
-        const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
+        const int ni = (int)(t / p.TdG) * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
         for (int kb = 0; kb < KB; ++kb) {
           TWAIT(0, empty + stage, phase ^ 1);
           if (p.debug & 2) {
             mbar_arrive(full + stage);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
-          mbar_arrive_expect_tx(full + stage, STAGE_TX);
+          } else {
+            mbar_arrive_expect_tx(full + stage, STAGE_TX);   // whole tiles: own + peers' slices
 #pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            tma_load_2d(sA + stage * CF::A_STAGE + l * A_LIMB_BYTES, &tmA, full + stage, kb * KE,
-                        (int)(l * p.Np + (int64_t)ni * BM));
-            tma_load_2d(sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES, &tmB, full + stage, kb * KE,
-                        (int)(l * p.Dq + (int64_t)di * BN));
+            for (int l = 0; l < NL; ++l) {
+              uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + rd * AR * KBYTES;
+              const int ya = (int)(l * p.Np + (int64_t)ni * BM + rd * AR);
+              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + rn * BR * KBYTES;
+              const int yb = (int)(l * p.Dq + (int64_t)di * BN + rn * BR);
+              if constexpr (CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, kb * KE, ya, a_mask);
+              else tma_load_2d(da, &tmA, full + stage, kb * KE, ya);
+              if constexpr (CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, kb * KE, yb, b_mask);
+              else tma_load_2d(db, &tmB, full + stage, kb * KE, yb);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -271,9 +322,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       int cs = 0;
       uint32_t cphase = 0;
       for (int64_t t = t0; t < t1; ++t) {
-        const int di = (int)(t % p.Td);
+        const int di = (int)(t % p.TdG) * CLD + rd;
         mbar_wait(cempty + cs, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));
+        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));   // + taus
         bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
         if constexpr (MODE == 2)
           bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
@@ -283,287 +334,321 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    // ===================================================== MMA issuer (whole warp, elected lane issues)
-    {
-      int stage = 0, buf = 0, hb = 0, cs = 0;
-      uint32_t phase = 0, bphase = 0, hphase = 0, cphase = 0, sphase = 0;
-      bool seg_first = true;
-      const uint32_t IDESC2 = make_idesc<0>(BM, (int)p.Kp);
-      const uint32_t d2 = tmem_base + CF::D2_COL;
-      // Stage II for tile tt: S += H(tt) [Chi(tt) + Clo(tt)]^T
-      auto stage2 = [&](int64_t tt) {
-        TWAIT(3, hfull + hb, hphase);
-        TWAIT(4, cfull + cs, cphase);
-        if (seg_first) TWAIT(5, sempty, sphase ^ 1);   // previous run's S drained
+    // ===================================================== Stage I MMA issuer (elected lane)
+    int stage = 0, buf = 0;
+    uint32_t phase = 0, bphase = 0;
+    const uint64_t a_desc0 = sdesc(smem_u32(sA));
+    const uint64_t b_desc0 = sdesc(smem_u32(sB));
+    for (int64_t t = t0; t < t1; ++t) {
+      TWAIT(1, tempty + buf, bphase ^ 1);
+      tc_fence_after();
+      const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
+      for (int kb = 0; kb < KB; ++kb) {
+        TWAIT(2, full + stage, phase);
         tc_fence_after();
-        const uint32_t h_base = smem_u32(sH + hb * H_BYTES);
-        const uint32_t c_base = smem_u32(sC + cs * CF::C_SLOT);
+        // descriptors = base descriptor + (byte offset >> 4) in the start-address field
+        const uint64_t a_d = a_desc0 + (uint64_t)((stage * CF::A_STAGE) >> 4);
+        const uint64_t b_d = b_desc0 + (uint64_t)((stage * CF::B_STAGE) >> 4);
+        if (!(p.debug & 1)) {
+          const uint32_t acc = (kb == 0) ? 0u : 1u;
+          if constexpr (MODE == 2) {
+            // The three B limb tiles are contiguous rows [b0; b1; b2] (240 x 64 B) and
+            // the accumulators contiguous columns [A0 | A1 | A2], so one MMA per A limb:
+            //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
+            // (each A tile is read from shared memory once per k-step, not 3 times).
 #pragma unroll
-        for (int s = 0; s < BN / 16; ++s) {
-          const uint64_t ad = smem_desc_interleaved(h_base + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            const uint64_t bd = smem_desc_interleaved(
-                c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
-            if (!(p.debug & 8)) tc_mma_elect<0>(d2, ad, bd, IDESC2, (seg_first && s == 0 && part == 0) ? 0u : 1u);
+            for (int ks = 0; ks < KBYTES / 32; ++ks)
+              tc_mma_i8x3_elect(acc0, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
+                                a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
+                                IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
+          } else {
+            static_assert(KBYTES / 32 == 4, "4 MMAs per stage");
+            tc_mma4_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
+                                IDESC, acc);
           }
         }
-        seg_first = false;
-        tc_commit_elect(hempty + hb);
-        tc_commit_elect(cempty + cs);
-        if (seg_last(tt, t1, p.Td)) {
-          tc_commit_elect(sfull);
-          seg_first = true;
-          sphase ^= 1;
+        if constexpr (CLS > 1) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
+        else tc_commit_elect(empty + stage);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
-        hb ^= 1;
-        if (hb == 0) hphase ^= 1;
-        cs ^= 1;
-        if (cs == 0) cphase ^= 1;
-      };
-      for (int64_t t = t0; t < t1; ++t) {
-        TWAIT(1, tempty + buf, bphase ^ 1);
-        tc_fence_after();
-        const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
-        const long long ts1 = clock64();
-        for (int kb = 0; kb < KB; ++kb) {
-          TWAIT(2, full + stage, phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * CF::A_STAGE);
-          const uint32_t b_base = smem_u32(sB + stage * CF::B_STAGE);
-#pragma unroll
-          for (int ks = 0; ks < ((p.debug & 1) ? 0 : KBYTES / 32); ++ks) {
-            const uint32_t acc = (kb == 0 && ks == 0) ? 0u : 1u;
-            if constexpr (MODE == 2) {
-              // The three B limb tiles are contiguous rows [b0; b1; b2] (240 x 64 B) and
-              // the accumulators contiguous columns [A0 | A1 | A2], so one MMA per A limb:
-              //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
-              // (each A tile is read from shared memory once per k-step, not 3 times).
-              const uint64_t bdesc = sdesc(b_base + ks * 32);
-              tc_mma_elect<2>(acc0, sdesc(a_base + ks * 32), bdesc, IDESC_N240, acc);
-              tc_mma_elect<2>(acc0 + BN, sdesc(a_base + A_LIMB_BYTES + ks * 32), bdesc,
-                        IDESC_N160, 1u);
-              tc_mma_elect<2>(acc0 + 2 * BN, sdesc(a_base + 2 * A_LIMB_BYTES + ks * 32), bdesc,
-                        IDESC, 1u);
-            } else {
-              tc_mma_elect<MODE>(acc0, sdesc(a_base + ks * 32), sdesc(b_base + ks * 32),
-                           IDESC, acc);
-            }
-          }
-          tc_commit_elect(empty + stage);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        tc_commit_elect(tfull + buf);
-        if (p.debug & 4) dbgc[13] += (unsigned long long)(clock64() - ts1);
-        buf ^= 1;
-        if (buf == 0) bphase ^= 1;
-        const long long ts2 = clock64();
-        if constexpr (!S2F)
-          if (t > t0) stage2(t - 1);        // overlaps the epilogue of tile t-1 with Stage I of t
-        if (p.debug & 4) dbgc[14] += (unsigned long long)(clock64() - ts2);
       }
-      if constexpr (!S2F)
-        if (t1 > t0) stage2(t1 - 1);
+      tc_commit_elect(tfull + buf);
+      buf ^= 1;
+      if (buf == 0) bphase ^= 1;
+    }
+  } else if (warp == 3) {
+    // ===================================================== Stage II MMA issuer (elected lane)
+    // A warp of its own: S += H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
+    // never waiting behind (or holding up) the Stage I issue loop.
+    int hb = 0, cs = 0;
+    uint32_t hphase = 0, cphase = 0, sphase = 0;
+    bool seg_first = true;
+    const uint32_t IDESC2 = make_idesc<0>(BM, (int)p.Kp);
+    const uint32_t d2 = tmem_base + CF::D2_COL;
+    for (int64_t t = t0; t < t1; ++t) {
+      TWAIT(3, hfull + hb, hphase);
+      TWAIT(4, cfull + cs, cphase);
+      if (seg_first) TWAIT(5, sempty, sphase ^ 1);
+      tc_fence_after();
+      const uint32_t c_base = smem_u32(sC + cs * CF::C_SLOT);
+#pragma unroll
+      for (int s = 0; s < BN / 16; ++s) {
+        const uint32_t acc = (seg_first && s == 0) ? 0u : 1u;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {      // C = hi + lo, both into the same columns
+          const uint64_t bd = smem_desc_interleaved(
+              c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
+          if (p.debug & 8) continue;
+          if constexpr (CF::H_TMEM) {
+            // A = H from TMEM (16 bf16 = 8 columns per k-step)
+            tc_mma_ts_elect(d2, tmem_base + CF::H_COL + hb * (BN / 2) + s * 8, bd, IDESC2,
+                            part == 0 ? acc : 1u);
+          } else {
+            const uint32_t h_base = smem_u32(sH + hb * CF::H_BYTES);
+            const uint64_t ad = smem_desc_interleaved(h_base + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
+            tc_mma_elect<0>(d2, ad, bd, IDESC2, part == 0 ? acc : 1u);
+          }
+        }
+      }
+      seg_first = false;
+      tc_commit_elect(hempty + hb);
+      tc_commit_elect(cempty + cs);
+      if (seg_last(t, t1, p.TdG)) {
+        tc_commit_elect(sfull);
+        seg_first = true;
+        sphase ^= 1;
+      }
+      if (++hb == NH) {
+        hb = 0;
+        hphase ^= 1;
+      }
+      cs ^= 1;
+      if (cs == 0) cphase ^= 1;
     }
   } else if (warp >= EPI_WARP0) {
     // ===================================================== epilogue
     const int ew = warp - EPI_WARP0;
     const int q = warp & 3;                 // TMEM lane quarter (hardware: warp id % 4)
-    const int cq = ew >> 2;                 // column quarter of the 80-wide tile
+    const int cq = ew >> 2;                 // column group of the tile
     const int m = q * 32 + lane;            // row within the N-tile
     const int K = (int)p.K;
     int buf = 0, hb = 0, cs = 0;
     uint32_t bphase = 0, hphase = 0, sphase = 0, cphase = 0;
     unsigned long long nrecheck = 0;
-    const int first_ni = (int)(t0 / p.Td);
-    float2 S2[KT / 2];                      // int8 mode: FFMA2 Stage II accumulators (this row)
-#pragma unroll
-    for (int k = 0; k < KT / 2; ++k) S2[k] = make_float2(0.f, 0.f);
-#define SK(k) (((k) & 1) ? S2[(k) >> 1].y : S2[(k) >> 1].x)
-    float* sRed = reinterpret_cast<float*>(sH);   // int8 mode: [K][BM] quarter reduction
+    const int first_ng = (int)(t0 / p.TdG);
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     for (int64_t t = t0; t < t1; ++t) {
-      const int ni = (int)(t / p.Td), di = (int)(t % p.Td);
+      const int ng = (int)(t / p.TdG);
+      const int ni = ng * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
       const int64_t row = (int64_t)ni * BM + m;
       const bool row_ok = row < p.N;
-      int64_t rtau = -1;                    // int8 mode: row part of tau (-1: padded row, never flag)
+      int64_t rtau = -1;                    // int8 mode: row part of tau
       if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : -(int64_t(1) << 62);
+      if (p.debug & 256) {                  // diagnostics: sleep-polling instead of try_wait
+        while (!mbar_test(tfull + buf, bphase)) __nanosleep(500);
+      }
       TWAIT(6, tfull + buf, bphase);
-      if constexpr (!S2F) TWAIT(7, hempty + hb, hphase ^ 1);
       const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
-      const float* sCt = nullptr;           // C^T tile [80][kpf] (int8 mode), in smem
-      if constexpr (S2F) {
+      if constexpr (MODE == 2) {
         TWAIT(15, cfull + cs, cphase);
-        sCt = reinterpret_cast<const float*>(sC + cs * CF::C_SLOT);
-        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + BN * KT * 4);
+        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
       }
       tc_fence_after();
-      uint8_t* hrow = sH + hb * H_BYTES + (m >> 3) * CORE_SBO + (m & 7) * 16;
-      const uint32_t tbase =
-          tmem_base + ((uint32_t)(q * 32) << 16) + buf * CF::ACC_STRIDE + cq * EPI_COLS;
-#pragma unroll 1
-      for (int ch = 0; ch < ((p.debug & 16) ? 0 : EPI_COLS / 4); ++ch) {
-        const int col0 = cq * EPI_COLS + ch * 4;   // column within the tile
-        uint32_t hbits = 0;                         // bit j set -> h = -1
+      // ---- phase 1: accumulator -> HardSign bits (bit set -> h = -1) and recheck flags
+      uint32_t hbits[NWB], flags[NWB];
+#pragma unroll
+      for (int w = 0; w < NWB; ++w) hbits[w] = flags[w] = 0u;
+      const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE + cq * EPI_COLS;
+#pragma unroll
+      for (int ch = 0; ch < ((p.debug & 16) ? 0 : EPI_COLS / CH); ++ch) {
+        const int cl = ch * CH;             // column within this thread's group
         if constexpr (MODE == 2) {
-          uint32_t r0[4], r1[4], r2[4];
-          tmem_ld4(tbase + ch * 4, r0);
-          tmem_ld4(tbase + BN + ch * 4, r1);
-          tmem_ld4(tbase + 2 * BN + ch * 4, r2);
-          tmem_ld_wait();
-          int64_t I[4];
-          uint32_t fl = 0;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            I[j] = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
-                   (int64_t)(int32_t)r2[j];
-            if (I[j] < 0) hbits |= 1u << j;
-            const int64_t aI = I[j] < 0 ? -I[j] : I[j];
-            if (aI <= rtau + sct[col0 + j]) fl |= 1u << j;   // coltau = -inf past D
+          uint32_t r0[CH], r1[CH], r2[CH];
+          if constexpr (CH == 16) {
+            tmem_ld16(tbase + cl, r0);
+            tmem_ld16(tbase + BN + cl, r1);
+            tmem_ld16(tbase + 2 * BN + cl, r2);
+          } else {
+            tmem_ld8(tbase + cl, r0);
+            tmem_ld8(tbase + BN + cl, r1);
+            tmem_ld8(tbase + 2 * BN + cl, r2);
           }
-          if (__any_sync(0xffffffffu, fl != 0)) {
-#pragma unroll 1
-            for (int j = 0; j < 4; ++j) {
-              unsigned mask = __ballot_sync(0xffffffffu, (fl >> j) & 1u);
-              const int64_t d = (int64_t)di * BN + col0 + j;
-              while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int64_t srow = (int64_t)ni * BM + q * 32 + src;
-                const float hv = recheck_warp(p, srow, d, lane);
-                if (lane == src) hbits = hv < 0.f ? (hbits | (1u << j)) : (hbits & ~(1u << j));
-                ++nrecheck;
-              }
-            }
-          }
-        } else {
-          uint32_t r0[4];
-          tmem_ld4(tbase + ch * 4, r0);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (!(__uint_as_float(r0[j]) >= 0.f)) hbits |= 1u << j;   // HardSign
-        }
-        if constexpr (S2F) {
-          // Stage II on the FMA pipe: S[k] += h[c] C[k, d0 + c], c ascending (exact +-1 products;
-          // padded columns have C = 0)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float h = ((hbits >> j) & 1u) ? -1.f : 1.f;
-            const float4* ct = reinterpret_cast<const float4*>(sCt + (col0 + j) * KT);  // kpf == KT
-#pragma unroll
-            for (int k4 = 0; k4 < KT / 4; ++k4) {
-              const float4 cv = ct[k4];
-              S2[2 * k4 + 0] = ffma2(h, make_float2(cv.x, cv.y), S2[2 * k4 + 0]);
-              S2[2 * k4 + 1] = ffma2(h, make_float2(cv.z, cv.w), S2[2 * k4 + 1]);
-            }
+          for (int j = 0; j < CH; ++j) {
+            const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
+                              (int64_t)(int32_t)r2[j];
+            const int b = cl + j;
+            if (I < 0) hbits[b >> 5] |= 1u << (b & 31);
+            const int64_t aI = I < 0 ? -I : I;
+            if (aI <= rtau + sct[cq * EPI_COLS + b]) flags[b >> 5] |= 1u << (b & 31);   // tau = -inf past D
           }
         } else {
-          // 4 bf16 +-1 values (0x3F80 / 0xBF80) -> 8 bytes of a core-matrix row
-          const uint32_t w0 = ((hbits & 1u) ? 0xBF80u : 0x3F80u) | (((hbits & 2u) ? 0xBF80u : 0x3F80u) << 16);
-          const uint32_t w1 = ((hbits & 4u) ? 0xBF80u : 0x3F80u) | (((hbits & 8u) ? 0xBF80u : 0x3F80u) << 16);
-          *reinterpret_cast<uint2*>(hrow + (col0 >> 3) * CORE_LBO + (col0 & 7) * 2) = make_uint2(w0, w1);
+          uint32_t r0[CH];
+          if constexpr (CH == 16) tmem_ld16(tbase + cl, r0);
+          else tmem_ld8(tbase + cl, r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int b = cl + j;
+            if (!(__uint_as_float(r0[j]) >= 0.f)) hbits[b >> 5] |= 1u << (b & 31);   // HardSign
+          }
         }
       }
       tc_fence_before();
-      if constexpr (!S2F) fence_proxy_async_smem();   // H writes -> visible to the tensor core
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(tempty + buf);
-        if constexpr (S2F) mbar_arrive(cempty + cs);
-        else mbar_arrive(hfull + hb);
+      if (lane == 0) mbar_arrive(tempty + buf);   // accumulator free for tile t + 2
+      // ---- phase 2 (int8 mode): float64 re-evaluation of the flagged signs
+      if constexpr (MODE == 2) {
+#pragma unroll
+        for (int w = 0; w < NWB; ++w) {
+          uint32_t fw = flags[w];
+          unsigned lanes = __ballot_sync(0xffffffffu, fw != 0u);
+          while (lanes) {
+            const int src = __ffs(lanes) - 1;
+            const int bit = __shfl_sync(0xffffffffu, __ffs(fw) - 1, src);
+            const int col = cq * EPI_COLS + w * 32 + bit;
+            const float hv = recheck_warp(p, (int64_t)ni * BM + q * 32 + src, (int64_t)di * BN + col, lane);
+            if (lane == src) {
+              hbits[w] = hv < 0.f ? (hbits[w] | (1u << bit)) : (hbits[w] & ~(1u << bit));
+              fw &= fw - 1;
+            }
+            ++nrecheck;
+            lanes = __ballot_sync(0xffffffffu, fw != 0u);
+          }
+        }
       }
+      // ---- phase 3: H (exact bf16 +-1: 0x3F80 / 0xBF80) for the Stage II MMA
+      TWAIT(7, hempty + hb, hphase ^ 1);
+      tc_fence_after();
+      if (p.debug & 128) {
+        // diagnostics: no H write
+      } else if constexpr (CF::H_TMEM) {
+        // packed bf16 pairs into TMEM columns H_COL + col / 2 of this thread's lane
+        const uint32_t hbase = tmem_base + lane_off + CF::H_COL + hb * (BN / 2) + cq * (EPI_COLS / 2);
+#pragma unroll
+        for (int g = 0; g < EPI_COLS / 16; ++g) {
+          uint32_t wv[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int b0 = g * 16 + 2 * j, b1 = b0 + 1;
+            const uint32_t lo = ((hbits[b0 >> 5] >> (b0 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            const uint32_t hi = ((hbits[b1 >> 5] >> (b1 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            wv[j] = lo | (hi << 16);
+          }
+          tmem_st8(hbase + g * 8, wv);
+        }
+        if constexpr (EPI_COLS % 16 != 0) {
+          // 8-column remainder (EPI_COLS = 40): four packed words
+          uint32_t wv[8];
+          const int g = EPI_COLS / 16;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int b0 = g * 16 + 2 * j, b1 = b0 + 1;
+            const uint32_t lo = ((hbits[b0 >> 5] >> (b0 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            const uint32_t hi = ((hbits[b1 >> 5] >> (b1 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            wv[j] = lo | (hi << 16);
+          }
+          tmem_st4(hbase + g * 8, wv);
+        }
+        tmem_st_wait();
+      } else {
+        uint8_t* hrow = sH + hb * CF::H_BYTES + (m >> 3) * CORE_SBO + (m & 7) * 16;
+#pragma unroll
+        for (int g = 0; g < EPI_COLS / 8; ++g) {
+          const int col0 = cq * EPI_COLS + g * 8;   // 8 columns = one 16-byte core-matrix row
+          uint32_t wv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int b0 = g * 8 + 2 * j, b1 = b0 + 1;
+            const uint32_t lo = ((hbits[b0 >> 5] >> (b0 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            const uint32_t hi = ((hbits[b1 >> 5] >> (b1 & 31)) & 1u) ? 0xBF80u : 0x3F80u;
+            wv[j] = lo | (hi << 16);
+          }
+          *reinterpret_cast<uint4*>(hrow + (col0 >> 3) * CORE_LBO) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        fence_proxy_async_smem();           // H writes -> visible to the tensor core
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(hfull + hb);
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
-      hb ^= 1;
-      if (hb == 0) hphase ^= 1;
+      if (++hb == NH) {
+        hb = 0;
+        hphase ^= 1;
+      }
       cs ^= 1;
       if (cs == 0) cphase ^= 1;
 
-      if (!seg_last(t, t1, p.Td)) continue;
-      // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM
-      const int c_first = owner_of((int64_t)ni * p.Td, p.T, p.G);
-      const int c_last = owner_of((int64_t)(ni + 1) * p.Td - 1, p.T, p.G);
-      const bool sole = (c_first == c_last);
-      constexpr int FIN = S2F ? NUM_CQ - 1 : 0;   // column group that finalises the run's scores
-      if constexpr (S2F) {
-        // fixed-order reduction of the 4 column quarters: ((S0 + S1) + S2) + S3
-        for (int qq = 0; qq < NUM_CQ - 1; ++qq) {
-          if (cq == qq) {
-#pragma unroll
-            for (int k = 0; k < KT; ++k)
-              if (k < K) sRed[k * BM + m] = (qq == 0) ? SK(k) : sRed[k * BM + m] + SK(k);
-          }
-          named_bar(1, NUM_EPI * 32);
-        }
-        if (cq == NUM_CQ - 1) {
-#pragma unroll
-          for (int k = 0; k < KT; ++k)
-            if (k < K) SK(k) = sRed[k * BM + m] + SK(k);
-        }
-      }
-      if (cq == FIN) {
-        if constexpr (!S2F) TWAIT(8, sfull, sphase);
+      if (!seg_last(t, t1, p.TdG)) continue;
+      // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM.  The
+      // N-tile's D-groups are split over clusters c_first..c_last, each over its CLD ranks.
+      const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G);
+      const int c_last = owner_of((int64_t)(ng + 1) * p.TdG - 1, p.T, p.G);
+      const bool sole = (c_first == c_last) && CLD == 1;
+      if (cq == 0) {
+        TWAIT(8, sfull, sphase);
         tc_fence_after();
-        const uint32_t sb = tmem_base + ((uint32_t)(q * 32) << 16) + CF::D2_COL;
-        float* part = p.S_part + (((int64_t)c * 2 + ((ni == first_ni) ? 0 : 1)) * BM + m) * p.K;
+        const uint32_t sb = tmem_base + lane_off + CF::D2_COL;
+        const int myslot = (CLD == 1) ? ((ng == first_ng) ? 0 : 1) : (ng - first_ng);
+        float* part = p.S_part + (((int64_t)c * p.nslot + myslot) * BM + m) * p.K;
         int best = 0;
         float bv = 0.f;
-        auto take = [&](float v, int k) {
-          if (sole) {
-            if (row_ok && p.scores) p.scores[row * p.K + k] = v;
-            if (k == 0 || v > bv) {
-              bv = v;
-              best = k;
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          uint32_t r[8];
+          tmem_ld8(sb + k0, r);
+          float v[8];
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            if (k < K) {
+              if (sole) {
+                if (row_ok && p.scores) p.scores[row * p.K + k] = v[j];
+                if (k == 0 || v[j] > bv) {
+                  bv = v[j];
+                  best = k;
+                }
+              } else {
+                part[k] = v[j];
+              }
             }
-          } else {
-            part[k] = v;
-          }
-        };
-        if constexpr (S2F) {
-#pragma unroll
-          for (int k = 0; k < KT; ++k)
-            if (k < K) take(SK(k), k);
-        } else {
-          for (int k0 = 0; k0 < K; k0 += 8) {
-            uint32_t r[8];
-            tmem_ld8(sb + k0, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (k0 + j < K) take(__uint_as_float(r[j]), k0 + j);
           }
         }
         tc_fence_before();
         __syncwarp();
-        if constexpr (!S2F)
-          if (lane == 0) mbar_arrive(sempty);
+        if (lane == 0) mbar_arrive(sempty);
         if (sole && row_ok && p.labels) p.labels[row] = best;
         if (!sole) __threadfence();
       }
-#pragma unroll
-      for (int k = 0; k < KT; ++k) SK(k) = 0.f;
       sphase ^= 1;
       if (sole) continue;
       named_bar(1, NUM_EPI * 32);
       if (threadIdx.x == EPI_WARP0 * 32) {
         const unsigned prev = atomicAdd(p.cnt + ni, 1u);
-        *s_flag = (prev == (unsigned)(c_last - c_first)) ? 1 : 0;
+        *s_flag = (prev == (unsigned)((c_last - c_first + 1) * CLD - 1)) ? 1 : 0;
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      if (*s_flag && cq == FIN && row_ok) {
+      if (*s_flag && cq == 0 && row_ok) {
         __threadfence();
         int best = 0;
         float bv = 0.f;
         for (int k = 0; k < K; ++k) {
           float s = 0.f;
-          for (int cc = c_first; cc <= c_last; ++cc) {
-            const int slot = ((int)(range_begin(cc, p.T, p.G) / p.Td) == ni) ? 0 : 1;
-            const float v = ld_cg(p.S_part + (((int64_t)cc * 2 + slot) * BM + m) * p.K + k);
-            s = (cc == c_first) ? v : s + v;
+          for (int cc = c_first; cc <= c_last; ++cc) {        // fixed order: cluster, then D rank
+            const int ng0 = (int)(range_begin(cc, p.T, p.G) / p.TdG);
+            const int slot = (CLD == 1) ? ((ng0 == ng) ? 0 : 1) : (ng - ng0);
+            for (int j = 0; j < CLD; ++j) {
+              const int64_t cta = (int64_t)cc * CLS + rn * CLD + j;
+              const float v = ld_cg(p.S_part + ((cta * p.nslot + slot) * BM + m) * p.K + k);
+              s = (cc == c_first && j == 0) ? v : s + v;
+            }
           }
           if (p.scores) p.scores[row * p.K + k] = s;
           if (k == 0 || s > bv) {
@@ -577,15 +662,15 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
-  if ((p.debug & 4) && lane == 0 && (warp <= 2 || warp == EPI_WARP0)) {
-    if (warp != 1) dbgc[13] = dbgc[14] = 0;
+  if ((p.debug & 4) && lane == 0 && (warp <= 3 || warp == EPI_WARP0)) {
     if (warp != EPI_WARP0) dbgc[15] = 0;
-    dbgc[9 + (warp == EPI_WARP0 ? 3 : warp)] = (unsigned long long)(clock64() - t_start);
+    dbgc[warp == EPI_WARP0 ? 12 : (warp == 3 ? 13 : 9 + warp)] = (unsigned long long)(clock64() - t_start);
     for (int i = 0; i < 16; ++i)
       if (dbgc[i]) atomicAdd(p.dbg + i, dbgc[i]);
   }
   __syncwarp();
-  __syncthreads();
+  if constexpr (CLS > 1) cluster_sync_all();   // no CTA leaves while peers may still signal it
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
@@ -667,11 +752,11 @@ __global__ void round_rows_kernel(const float* __restrict__ src, int64_t rows, i
 
 
 // C tiles for Stage II: per D-tile di, bf16 hi = RN(C), lo = RN(C - hi), each
-// [Kp][80] in the interleaved K-major core-matrix layout the MMA B descriptor
-// expects (core matrix (g, j) = rows 8g.., columns 8j.. at byte (10 g + j) * 128).
+// [Kp][bn] in the interleaved K-major core-matrix layout the MMA B descriptor
+// expects (core matrix (g, j) = rows 8g.., columns 8j.. at byte (g bn/8 + j) * 128).
 __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int64_t Kp, int64_t D,
-                                    int64_t Dp, int64_t Td, __nv_bfloat16* __restrict__ out) {
-  const int64_t per_part = Kp * BN;
+                                    int64_t Dp, int64_t Td, int bn, __nv_bfloat16* __restrict__ out) {
+  const int64_t per_part = Kp * bn;
   const int64_t total = Td * 2 * per_part;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -679,24 +764,12 @@ __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int
     const int part = (int)((i / per_part) % 2);
     const int64_t e = i % per_part;          // element index inside the interleaved part
     const int64_t core = e / 64, inner = e % 64;
-    const int64_t g = core / (BN / 8), j = core % (BN / 8);
+    const int64_t g = core / (bn / 8), j = core % (bn / 8);
     const int64_t r = g * 8 + inner / 8, cc = j * 8 + inner % 8;
-    const int64_t d = di * BN + cc;
+    const int64_t d = di * bn + cc;
     const float v = (r < K && d < D) ? Cp[r * Dp + d] : 0.f;
     const __nv_bfloat16 hi = __float2bfloat16_rn(v);
     out[i] = part == 0 ? hi : __float2bfloat16_rn(v - __bfloat162float(hi));
-  }
-}
-
-// int8 mode Stage II operand: fp32 C^T tiles [Td][80][kpf] (row = column d of the tile,
-// classes contiguous, zero beyond K and beyond D).
-__global__ void ct_tiles_kernel(const float* __restrict__ Cp, int64_t K, int64_t kpf, int64_t D,
-                                int64_t Dp, int64_t Td, float* __restrict__ out) {
-  const int64_t total = Td * BN * kpf;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = i % kpf, dd = i / kpf;      // dd = global column index di * 80 + c
-    out[i] = (k < K && dd < D) ? Cp[k * Dp + dd] : 0.f;
   }
 }
 
@@ -731,24 +804,88 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int KT>
-cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, cudaStream_t st) {
-  const size_t sm = Cfg<MODE>::TOTAL + 1024;
-  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE, KT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <int MODE, int BN, int CLN, int CLD>
+cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p, int num_sms,
+                        cudaStream_t st) {
+  constexpr int CLS = CLN * CLD;
+  const size_t sm = Cfg<MODE, BN>::TOTAL + 1024;
+  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  fused_tc_kernel<MODE, KT><<<p.G, THREADS, sm, st>>>(a, b, p);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CLS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent: as many clusters as can be co-resident (148 SMs: 74 pairs, 33 quads)
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cfg.gridDim = dim3(CLS * (num_sms / CLS), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = num_sms / CLS;
+    }
+    max_clusters = n;
+  }
+  p.G = (int)(p.T < max_clusters ? p.T : max_clusters);
+  const int64_t per = (p.T + p.G - 1) / p.G;    // cluster tiles per range (at most)
+  p.nslot = (CLD == 1) ? 2 : (int)((per + p.TdG - 1) / p.TdG + 1);
+  if ((int64_t)p.G * CLS * p.nslot > p.s_part_cap) return cudaErrorInvalidValue;   // workspace bound
+  cfg.gridDim = dim3(p.G * CLS, 1, 1);
+  e = cudaLaunchKernelEx(&cfg, kern, a, b, (const TcParams)p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <int MODE, int BN>
+cudaError_t launch_cluster(int cl_n, int cl_d, const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
+                           int num_sms, cudaStream_t st) {
+  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1>(a, b, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2>(a, b, p, num_sms, st);
+  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1>(a, b, p, num_sms, st);
+  if (cl_n == 2 && cl_d == 2) return launch_mode<MODE, BN, 2, 2>(a, b, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4>(a, b, p, num_sms, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-int tc_tile_n() { return BN; }
+int tc_tile_n(int mode, int64_t K) { return tile_n_for(mode, K); }
+int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int num_sms) {
+  if (cl_d == 1) return 2 * (int64_t)num_sms;
+  const int64_t T = (Tn / cl_n) * (Td / cl_d), TdG = Td / cl_d;
+  const int64_t gmin = num_sms / (cl_n * cl_d) / 2 > 0 ? num_sms / (cl_n * cl_d) / 2 : 1;  // >= half co-resident
+  const int64_t per = (T + gmin - 1) / gmin;
+  return (int64_t)num_sms * ((per + TdG - 1) / TdG + 1);
+}
+void tc_cluster_shape(int mode, int64_t K, int* cl_n, int* cl_d) {
+  // default: CTA pairs on two N-tiles of the same D-tile, multicasting the B tile
+  // (measured best of 1x1 / 1x2 / 2x1 / 2x2 / 1x4 at cfg2, tools/tc_timing.py)
+  int n = 2, d = 1;
+  if (tile_n_for(mode, K) == 80 && mode != 2) n = 1;   // (bf16/tf32 with K > 32: no cluster)
+  const char* env = getenv("HDC_TC_CLUSTER");
+  int en = 0, ed = 0;
+  if (env && sscanf(env, "%dx%d", &en, &ed) == 2 &&
+      ((en == 1 && (ed == 1 || ed == 2 || ed == 4)) || (en == 2 && (ed == 1 || ed == 2))) &&
+      !(tile_n_for(mode, K) == 80 && mode != 2)) {
+    n = en;
+    d = ed;
+  }
+  *cl_n = n;
+  *cl_d = d;
+}
 int tc_max_k(int mode) { return mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
 int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
-int64_t tc_kpf(int64_t K) { return (K + 3) / 4 * 4; }
 int64_t tc_c_tile_bytes(int mode, int64_t K) {
-  return mode == 2 ? BN * tc_kpf(K) * 4 : 2 * tc_kp(K) * BN * 2;
+  const int64_t bn = tile_n_for(mode, K);
+  return 2 * tc_kp(K) * bn * 2;            // bf16 hi + lo, [Kp][bn] each
 }
 int64_t tc_max_fp_int8() { return 100000; }
 
@@ -778,33 +915,23 @@ cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t ro
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, void* out,
-                              cudaStream_t st) {
-  const int64_t Td = (D + BN - 1) / BN;
-  if (mode == 2) {
-    const int64_t total = Td * BN * tc_kpf(K);
-    int64_t grid = (total + 255) / 256;
-    if (grid > 148 * 16) grid = 148 * 16;
-    ct_tiles_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, tc_kpf(K), D, Dp, Td, (float*)out);
-    return cudaGetLastError();
-  }
-  return launch_tc_c_interleave(Cp, K, tc_kp(K), D, Dp, out, st);
-}
-
-cudaError_t launch_tc_c_interleave(const float* Cp, int64_t K, int64_t Kp, int64_t D, int64_t Dp,
-                                   void* out, cudaStream_t st) {
-  const int64_t Td = (D + BN - 1) / BN;
-  const int64_t total = Td * 2 * Kp * BN;
+cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, int64_t Dq,
+                              void* out, cudaStream_t st) {
+  const int bn = tile_n_for(mode, K);
+  const int64_t Td = Dq / bn;                 // includes cluster padding tiles (all zero)
+  const int64_t Kp = tc_kp(K);
+  const int64_t total = Td * 2 * Kp * bn;
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
-  c_interleave_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, Kp, D, Dp, Td, (__nv_bfloat16*)out);
+  c_interleave_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, Kp, D, Dp, Td, bn, (__nv_bfloat16*)out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st) {
-  const int64_t Tn = o.N_p / BM;
-  const int64_t Td = (o.D + BN - 1) / BN;
+  const int bn = tile_n_for(mode, o.K);
+  const int64_t Tn = o.N_p / BM;              // multiple of cl_n
+  const int64_t Td = o.Dq / bn;               // multiple of cl_d
   TcParams p;
   p.N = N;
   p.F = o.F;
@@ -817,16 +944,17 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.Np = o.N_p;
   p.Tn = (int)Tn;
   p.Td = (int)Td;
-  p.T = Tn * Td;
-  p.G = (int)(p.T < num_sms ? p.T : num_sms);
+  p.TdG = (int)(Td / o.cl_d);
+  p.T = (Tn / o.cl_n) * p.TdG;
+  p.G = 0;                                    // set by launch_mode (co-resident clusters)
   p.X = o.X;
   p.Bt = o.Bt;
   p.rowtau = o.rowtau;
   p.coltau = o.coltau;
   p.Cil = (const uint8_t*)o.Cil;
-  p.kpf = (int)tc_kpf(o.K);
   p.c_tile_bytes = (uint32_t)tc_c_tile_bytes(mode, o.K);
   p.S_part = o.S_part;
+  p.s_part_cap = o.s_part_slots;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
   p.scores = scores;
@@ -850,27 +978,24 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   CUtensorMap ma, mb;
   const uint32_t kbytes = (mode == 2) ? 64 : 128;
   const CUtensorMapSwizzle swz = (mode == 2) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, BM, swz) ||
-      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, BN, swz))
+  // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
+  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, BM / o.cl_d, swz) ||
+      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, bn / o.cl_n, swz))
     return cudaErrorInvalidValue;
   cudaError_t e;
-  if (mode == 0) e = launch_mode<0, 4>(ma, mb, p, st);
-  else if (mode == 1) e = launch_mode<1, 4>(ma, mb, p, st);
-  else if (p.kpf <= 4) e = launch_mode<2, 4>(ma, mb, p, st);
-  else if (p.kpf <= 8) e = launch_mode<2, 8>(ma, mb, p, st);
-  else if (p.kpf <= 12) e = launch_mode<2, 12>(ma, mb, p, st);
-  else if (p.kpf <= 16) e = launch_mode<2, 16>(ma, mb, p, st);
-  else if (p.kpf <= 20) e = launch_mode<2, 20>(ma, mb, p, st);
-  else if (p.kpf <= 24) e = launch_mode<2, 24>(ma, mb, p, st);
-  else if (p.kpf <= 28) e = launch_mode<2, 28>(ma, mb, p, st);
-  else e = launch_mode<2, 32>(ma, mb, p, st);
+  if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
+  else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
+  else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
+  else if (o.cl_n == 1 && o.cl_d == 1)
+    e = (mode == 0) ? launch_mode<0, 80, 1, 1>(ma, mb, p, num_sms, st) : launch_mode<1, 80, 1, 1>(ma, mb, p, num_sms, st);
+  else e = cudaErrorInvalidValue;
   if (e == cudaSuccess && (p.debug & 4)) {
     unsigned long long h[16];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost);
-    const char* names[16] = {"prod.empty", "mma.tempty", "mma.full", "mma.hfull", "mma.cfull",
-                             "mma.sempty", "epi.tfull", "epi.hempty", "epi.sfull", "prod.total",
-                             "mma.total", "cprod.total", "epi.total", "mma.SI", "mma.SII", "epi.cfull"};
+    const char* names[16] = {"prod.empty", "mma.tempty", "mma.full", "s2.hfull", "s2.cfull",
+                             "s2.sempty", "epi.tfull", "epi.hempty", "epi.sfull", "prod.total",
+                             "mma.total", "cprod.total", "epi.total", "s2.total", "-", "epi.cfull"};
     fprintf(stderr, "[hdc tc debug] mode %d, %d CTAs, %lld tiles; mean cycles per CTA:", mode, p.G,
             (long long)p.T);
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / p.G);

@@ -57,7 +57,8 @@ cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, cons
 
 // K4: fused tcgen05 kernel.  mode 0 = bf16, 1 = tf32, 2 = int8x3 (sign-exact).
 struct TcOperands {
-  int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to the 80-column tile; N_p to 128 rows
+  int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to cl_d D-tiles; N_p to cl_n x 128 rows
+  int cl_n, cl_d;                    // thread-block cluster shape (N-tiles x D-tiles), multicast
   const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
   const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
   const void* Cil;                   // per D-tile Stage II operand (tc_c_tile_bytes each)
@@ -65,17 +66,21 @@ struct TcOperands {
   const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
   const int64_t* rowtau;             // [N_p] int8 mode
   const int64_t* coltau;             // [Dq]  int8 mode
-  float* S_part;                     // [num_sms][2][128][K]
+  float* S_part;                     // [s_part_slots][128][K]
+  int64_t s_part_slots;
   unsigned* cnt;                     // [N_p / 128]
   unsigned long long* recheck;
 };
-int tc_tile_n();
+int tc_tile_n(int mode, int64_t K);   // D-tile width of K4 (80 or 160)
+// Cluster shape of K4 for a mode (HDC_TC_CLUSTER="NxD" overrides, for measurements).
+void tc_cluster_shape(int mode, int64_t K, int* cl_n, int* cl_d);
+// Partial-score slots ([128][K] each) K4 needs for Tn x Td tiles with that cluster shape.
+int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int num_sms);
 int tc_max_k(int mode);
 int64_t tc_kp(int64_t K);
-int64_t tc_kpf(int64_t K);
 int64_t tc_c_tile_bytes(int mode, int64_t K);
-cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, void* out,
-                              cudaStream_t st);
+cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, int64_t Dp, int64_t Dq,
+                              void* out, cudaStream_t st);
 int64_t tc_max_fp_int8();
 int64_t tc_tau_const(int64_t F);
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
@@ -83,8 +88,6 @@ cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int6
                             cudaStream_t st);
 cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t rows_p, int64_t F,
                             int64_t ld_src, int64_t Fp, void* out, cudaStream_t st);
-cudaError_t launch_tc_c_interleave(const float* Cp, int64_t K, int64_t Kp, int64_t D, int64_t Dp,
-                                   void* out, cudaStream_t st);
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st);
 

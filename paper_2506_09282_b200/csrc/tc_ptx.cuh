@@ -29,8 +29,33 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// HDC_MBAR_WAIT: 0 = try_wait (may suspend), 1 = test_wait spin, 2 = try_wait with a
+// short suspend-time hint (HDC_MBAR_HINT_NS).
+#ifndef HDC_MBAR_WAIT
+#define HDC_MBAR_WAIT 0
+#endif
+#ifndef HDC_MBAR_HINT_NS
+#define HDC_MBAR_HINT_NS 20
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#if HDC_MBAR_WAIT == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+#elif HDC_MBAR_WAIT == 2
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity), "n"(HDC_MBAR_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -38,6 +63,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
+}
+
+// Non-blocking probe: true iff the phase with parity `parity` has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Bounded wait: true once the phase completed, false after ~`ns` nanoseconds (the thread
+// may be suspended meanwhile instead of spinning on the barrier unit).
+__device__ __forceinline__ bool mbar_try_wait_ns(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
+// Warp-uniform probe (lane 0 decides): keeps the MMA warp converged for elect.sync.
+__device__ __forceinline__ bool mbar_test_uniform(uint64_t* bar, uint32_t parity) {
+  return __shfl_sync(0xffffffffu, mbar_test(bar, parity) ? 1 : 0, 0) != 0;
 }
 
 // ---------------------------------------------------------------- TMA
@@ -51,6 +109,28 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* desc, ui
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// Multicast variant: the box lands at the same shared-memory offset in every CTA of
+// `mask` (cluster ranks) and completes tx bytes on the mbarrier at `bar`'s offset in each.
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* desc, uint64_t* bar, int c0,
+                                               int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- clusters
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {  // every thread of every CTA of the cluster
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 
 // 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
@@ -145,11 +225,68 @@ __device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint64_t adesc, ui
         : "memory");
   }
 }
+// One stage of Stage I in a single elected issue: 4 MMAs D (+)= A_k B_k^T (k = 0..3),
+// the first accumulating iff `accumulate`.  One elect and all descriptors in uniform
+// registers up front, so the four UTCHMMA issue back to back.
+template <int KIND>
+__device__ __forceinline__ void tc_mma4_elect(uint32_t d, uint64_t a0, uint64_t b0, uint64_t a1, uint64_t b1,
+                                              uint64_t a2, uint64_t b2, uint64_t a3, uint64_t b3,
+                                              uint32_t idesc, uint32_t accumulate) {
+#define HDC_MMA4(KS)                                                                          \
+  asm volatile(                                                                             \
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %10, 0;\n\t"   \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %1, %2, %9, p;\n\t"                           \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %3, %4, %9, 1;\n\t"                           \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %5, %6, %9, 1;\n\t"                           \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %7, %8, %9, 1;\n\t}" ::"r"(d),                \
+      "l"(a0), "l"(b0), "l"(a1), "l"(b1), "l"(a2), "l"(b2), "l"(a3), "l"(b3), "r"(idesc),      \
+      "r"(accumulate)                                                                          \
+      : "memory")
+  if constexpr (KIND == 0) HDC_MMA4("kind::f16");
+  else if constexpr (KIND == 1) HDC_MMA4("kind::tf32");
+  else HDC_MMA4("kind::i8");
+#undef HDC_MMA4
+}
+
+// One int8 k-step of the 3-limb scheme (see k_fused_tc.cu): three MMAs, one elect.
+__device__ __forceinline__ void tc_mma_i8x3_elect(uint32_t d0, uint64_t a0, uint64_t a1, uint64_t a2,
+                                                  uint64_t b, uint32_t i240, uint32_t i160, uint32_t i80,
+                                                  uint32_t dcol, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 d1, d2;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\tadd.u32 d1, %0, %7;\n\tadd.u32 d2, d1, %7;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], %2, %4, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], %3, %4, %9, 1;\n\t}" ::"r"(d0),
+      "l"(a0), "l"(a1), "l"(a2), "l"(b), "r"(i240), "r"(i160), "r"(dcol), "r"(accumulate), "r"(i80)
+      : "memory");
+}
+
+// A operand from TMEM (kind::f16, K-major: lane = row, 2 bf16 per 32-bit column,
+// element k of a K=16 step at column k/2, low half for even k), B from shared memory.
+__device__ __forceinline__ void tc_mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+
+// Commit arriving on the mbarrier at `bar`'s offset in every CTA of `mask`.
+__device__ __forceinline__ void tc_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 
@@ -166,6 +303,31 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr));
+}
+// 32 lanes x 32-bit, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// 32 lanes x 32-bit stores, 8 consecutive columns per thread (registers -> TMEM).
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[8]) {  // r[0..3]
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");

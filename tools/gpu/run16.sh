@@ -1,0 +1,3 @@
+SHAPES=1x1,2x1 FLAGS=0,27,26 PRECS=bf16,fp32_tc,tf32 timeout 300 python tools/tc_timing.py 2>&1 | grep -v "^\[hdc" | tail -18
+SHAPES=1x1 FLAGS=4,31 PRECS=bf16 timeout 300 python tools/tc_timing.py 2>&1 | grep "^\[hdc" | sort | uniq | tail -2
+timeout 300 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -2
