@@ -35,6 +35,12 @@ HDC_DEV float2 ffma2(float a, float2 b, float2 c) {
   return r;
 }
 
+HDC_DEV float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 template <typename T>
 HDC_DEV T warp_sum_xor(T v) {
 #pragma unroll

@@ -59,6 +59,14 @@ struct hdc_model_s {
   // tensor-core workspace, grown with N
   int64_t tw_rows = 0;
   int64_t tw_slots = 0;      // capacity of S_part_tc in [128][K] slots
+  // int8 mode deferred rechecks: listed signs, fixed-point corrections, affected rows
+  int corr_shift = 0;
+  uint2* flags = nullptr;
+  unsigned long long* flag_count = nullptr;
+  unsigned long long flag_cap = 0;
+  long long* corr = nullptr;          // [tw_rows][Kp]
+  unsigned* dirty = nullptr;          // [tw_rows]
+  float* S_ws = nullptr;              // [tw_rows][K] scores when the caller passes none
   void* Atc = nullptr;       // [NL][Np][Fp]
   int64_t* rowtau = nullptr; // [Np]
   float* S_part_tc = nullptr;
@@ -118,7 +126,7 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
   if (F < 1 || D < 1 || K < 1) return fail(HDC_ERR_INVALID_VALUE, "F, D, K must be >= 1");
   if (K > HDC_MAX_K) return fail(HDC_ERR_INVALID_VALUE, "K > HDC_MAX_K (256)");
   if (F > kMaxF) return fail(HDC_ERR_UNSUPPORTED, "F > 2^20 (sign-recheck bound validity)");
-  if (D > (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "D > 2^31");
+  if (D > (int64_t(1) << 31) - 4096) return fail(HDC_ERR_UNSUPPORTED, "D > 2^31 - 4096");
   return HDC_OK;
 }
 
@@ -132,6 +140,11 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->rowtau);
   cudaFree(m->S_part_tc);
   cudaFree(m->cnt_tc);
+  cudaFree(m->flags);
+  cudaFree(m->flag_count);
+  cudaFree(m->corr);
+  cudaFree(m->dirty);
+  cudaFree(m->S_ws);
   cudaFree(m->Bp);
   cudaFree(m->Bt);
   cudaFree(m->B4);
@@ -211,7 +224,13 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   cudaFree(m->rowtau);
   cudaFree(m->S_part_tc);
   cudaFree(m->cnt_tc);
+  cudaFree(m->flags);
+  cudaFree(m->flag_count);
+  cudaFree(m->corr);
+  cudaFree(m->dirty);
+  cudaFree(m->S_ws);
   m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->cnt_tc = nullptr;
+  m->flags = nullptr; m->flag_count = nullptr; m->corr = nullptr; m->dirty = nullptr; m->S_ws = nullptr;
   m->tw_rows = 0;
   m->tw_slots = 0;
   cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * rows * m->Fp);
@@ -219,6 +238,23 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * nsl * kTileM * m->K);
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (rows / kTileM));
+  if (e == cudaSuccess && mode == 2) {
+    // list capacity: ~1/256 of the elements (measured ~1e-4 flagged), at most 4M entries;
+    // beyond it the kernel re-evaluates inline (correct, slower)
+    const int64_t kp = tc_kp(m->K);
+    unsigned long long cap = (unsigned long long)(rows * m->Dq / 256);
+    if (cap < (1ull << 16)) cap = 1ull << 16;
+    if (cap > (1ull << 22)) cap = 1ull << 22;
+    e = cudaMalloc((void**)&m->flags, sizeof(uint2) * cap);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->flag_count, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(m->flag_count, 0, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->corr, sizeof(long long) * rows * kp);
+    if (e == cudaSuccess) e = cudaMemset(m->corr, 0, sizeof(long long) * rows * kp);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->dirty, sizeof(unsigned) * rows);
+    if (e == cudaSuccess) e = cudaMemset(m->dirty, 0, sizeof(unsigned) * rows);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_ws, sizeof(float) * rows * m->K);
+    m->flag_cap = cap;
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(HDC_ERR_NO_MEMORY, "tensor-core workspace allocation");
@@ -262,11 +298,24 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.s_part_slots = m->tw_slots;
   o.cnt = m->cnt_tc;
   o.recheck = m->recheck;
+  o.Cp = m->Cp;
+  o.flags = m->flags;
+  o.flag_count = m->flag_count;
+  o.flag_cap = m->flag_cap;
+  o.corr = m->corr;
+  o.dirty = m->dirty;
+  // int8 mode: the fused kernel always writes (provisional) scores, corrected afterwards
+  float* S = (mode == 2 && !scores) ? m->S_ws : scores;
   m->tic(st);
-  e = launch_fused_tc(mode, o, N, scores, labels, m->num_sms, st);
+  e = launch_fused_tc(mode, o, N, S, labels, m->num_sms, st);
   m->toc(st);
   if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
   m->last_launches = 2;
+  if (mode == 2) {
+    e = launch_tc_recheck(o, N, S, labels, m->corr_shift, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tc recheck launch");
+    m->last_launches = 4;
+  }
   return HDC_OK;
 }
 
@@ -323,6 +372,7 @@ hdc_status_t validate_call(hdc_model_s* m, const float* X, int64_t N, const void
                            const void* out_optional) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
   if (N < 0) return fail(HDC_ERR_INVALID_VALUE, "N < 0");
+  if (N >= (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "N >= 2^31 (row indices are 32-bit)");
   if (N > 0 && (!X || !out_required)) return fail(HDC_ERR_INVALID_VALUE, "null X or output");
   if (!aligned(X, 4) || !aligned(out_required, 4) || !aligned(out_optional, 4))
     return fail(HDC_ERR_MISALIGNED, "pointers must be 4-byte aligned");
@@ -412,6 +462,10 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
     if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Dq, m->Cil, st0);
+    if (e == cudaSuccess && mode == 2) {
+      e = cudaDeviceSynchronize();
+      if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
+    }
   }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

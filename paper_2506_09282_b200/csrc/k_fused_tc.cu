@@ -36,6 +36,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <cmath>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -134,6 +136,9 @@ struct TcParams {
                            // else one per N-group of the cluster's range
   unsigned* cnt;           // [Tn]
   unsigned long long* recheck_count;
+  uint2* flags;                     // int8 mode: (row, d | provisional-negative << 31) to re-evaluate
+  unsigned long long* flag_count;   // appended entries (may exceed flag_cap: overflow re-evaluated inline)
+  unsigned long long flag_cap;
   float* scores;
   int32_t* labels;
   int debug;               // diagnostics only (HDC_TC_DEBUG): 1 = no Stage I MMA, 2 = no operand TMA,
@@ -166,12 +171,11 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 
 // float64 re-evaluation of V[row, d] (fixed lane order, warp-cooperative).
-__device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, int64_t d, int lane) {
-  const float* xr = p.X + row * p.F;
-  const float* br = p.Bt + d * p.Fp;
+__device__ __forceinline__ float recheck_dot(const float* __restrict__ xr, const float* __restrict__ br,
+                                             int64_t F, int lane) {
   double s = 0.0;
   int64_t f = lane;
-  for (; f + 96 < p.F; f += 128) {       // 8 independent loads in flight, then the FMAs in f order
+  for (; f + 96 < F; f += 128) {         // 8 independent loads in flight, then the FMAs in f order
     float xv[4], bv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -181,9 +185,12 @@ __device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, in
 #pragma unroll
     for (int u = 0; u < 4; ++u) s = fma((double)xv[u], (double)bv[u], s);
   }
-  for (; f < p.F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
+  for (; f < F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
   s = warp_sum_xor(s);
   return s >= 0.0 ? 1.f : -1.f;
+}
+__device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, int64_t d, int lane) {
+  return recheck_dot(p.X + row * p.F, p.Bt + d * p.Fp, p.F, lane);
 }
 
 __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
@@ -500,29 +507,46 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);   // accumulator free for tile t + 2
-      // ---- phase 2 (int8 mode): float64 re-evaluation of the flagged signs
+      // H buffer hb free (Stage II of tile t - 2 done; its recheck queue drained)
+      TWAIT(7, hempty + hb, hphase ^ 1);
+      tc_fence_after();
+      // ---- phase 2 (int8 mode): flagged signs are appended to a global list with the
+      // provisional sign used in H; hdc_recheck_kernel re-evaluates them in float64 after
+      // this kernel and corrects S exactly where a sign flips (Stage II is linear in H).
+      // Only a list overflow (e.g. many all-zero rows) falls back to re-evaluating here.
       if constexpr (MODE == 2) {
 #pragma unroll
         for (int w = 0; w < NWB; ++w) {
-          uint32_t fw = flags[w];
-          unsigned lanes = __ballot_sync(0xffffffffu, fw != 0u);
+          uint32_t fw = (p.debug & 512) ? 0u : flags[w];   // 512: diagnostics, no rechecks
+          uint32_t spill = 0u;
+          while (fw) {
+            const int bit = __ffs(fw) - 1;
+            fw &= fw - 1;
+            const int col = cq * EPI_COLS + w * 32 + bit;
+            const unsigned long long slot = atomicAdd(p.flag_count, 1ull);
+            if (slot < p.flag_cap) {
+              const uint32_t neg = (hbits[w] >> bit) & 1u;
+              p.flags[slot] = make_uint2((uint32_t)row, (uint32_t)((int64_t)di * BN + col) | (neg << 31));
+            } else {
+              spill |= 1u << bit;
+            }
+          }
+          unsigned lanes = __ballot_sync(0xffffffffu, spill != 0u);
           while (lanes) {
             const int src = __ffs(lanes) - 1;
-            const int bit = __shfl_sync(0xffffffffu, __ffs(fw) - 1, src);
+            const int bit = __shfl_sync(0xffffffffu, __ffs(spill) - 1, src);
             const int col = cq * EPI_COLS + w * 32 + bit;
             const float hv = recheck_warp(p, (int64_t)ni * BM + q * 32 + src, (int64_t)di * BN + col, lane);
             if (lane == src) {
               hbits[w] = hv < 0.f ? (hbits[w] | (1u << bit)) : (hbits[w] & ~(1u << bit));
-              fw &= fw - 1;
+              spill &= spill - 1;
             }
             ++nrecheck;
-            lanes = __ballot_sync(0xffffffffu, fw != 0u);
+            lanes = __ballot_sync(0xffffffffu, spill != 0u);
           }
         }
       }
       // ---- phase 3: H (exact bf16 +-1: 0x3F80 / 0xBF80) for the Stage II MMA
-      TWAIT(7, hempty + hb, hphase ^ 1);
-      tc_fence_after();
       if (p.debug & 128) {
         // diagnostics: no H write
       } else if constexpr (CF::H_TMEM) {
@@ -773,6 +797,74 @@ __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int
   }
 }
 
+// ---------------------------------------------------------------- int8 mode: deferred rechecks
+// (1) One warp per listed sign: float64 re-evaluation (the same fixed-order sum as the
+// in-kernel fallback).  Where it differs from the provisional sign that went into H,
+// S[row, :] is off by exactly (h - h') C[:, d] = 2 h C[:, d] (Stage II is linear in H,
+// P:180-183); that correction is accumulated in int64 fixed point (2^-shift units), so
+// the sum is exact and independent of the order the warps run in: bit-deterministic.
+__global__ void tc_recheck_kernel(const float* __restrict__ X, const float* __restrict__ Bt, int64_t F,
+                                  int64_t Fp, const float* __restrict__ Cp, int64_t Dp, int64_t K,
+                                  int64_t Kp, const uint2* __restrict__ flags,
+                                  const unsigned long long* __restrict__ flag_count,
+                                  unsigned long long cap, int shift, long long* __restrict__ corr,
+                                  unsigned* __restrict__ dirty, unsigned long long* recheck_count) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long cnt = *flag_count;
+  const unsigned long long n = cnt < cap ? cnt : cap;
+  const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+  const double scale = ldexp(2.0, shift);
+  for (unsigned long long i = w0; i < n; i += nw) {
+    const uint2 e = flags[i];
+    const int64_t row = e.x, d = e.y & 0x7FFFFFFFu;
+    const bool neg_prov = (e.y >> 31) != 0u;
+    const float hv = recheck_dot(X + row * F, Bt + d * Fp, F, lane);
+    if ((hv < 0.f) != neg_prov) {
+      if (lane == 0) dirty[row] = 1u;
+      for (int64_t k = lane; k < K; k += 32) {
+        const double c = (double)__ldg(Cp + k * Dp + d) * scale;
+        atomicAdd(reinterpret_cast<unsigned long long*>(corr + row * Kp + k),
+                  (unsigned long long)(long long)llrint(hv < 0.f ? -c : c));
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(recheck_count, n);
+}
+
+// (2) Rows with a flipped sign: S = S' + corr 2^-shift, lowest-index argmax;
+// clears the row's workspace and the list for the next call.
+__global__ void tc_finalize_kernel(int64_t N, int64_t K, int64_t Kp, int shift, float* __restrict__ S,
+                                   long long* __restrict__ corr, unsigned* __restrict__ dirty,
+                                   int32_t* __restrict__ labels, unsigned long long* flag_count) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row == 0) *flag_count = 0ull;        // the recheck kernel has read it (stream order)
+  if (row >= N || !dirty[row]) return;
+  const double inv = ldexp(1.0, -shift);
+  int best = 0;
+  float bv = 0.f;
+  for (int64_t k = 0; k < K; ++k) {
+    const float v = (float)((double)S[row * K + k] + (double)corr[row * Kp + k] * inv);
+    S[row * K + k] = v;
+    corr[row * Kp + k] = 0;
+    if (k == 0 || v > bv) {
+      bv = v;
+      best = (int)k;
+    }
+  }
+  if (labels) labels[row] = best;
+  dirty[row] = 0u;
+}
+
+// max |C| over the model (for the fixed-point shift of the corrections)
+__global__ void absmax_kernel(const float* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(a[i]));
+  m = warp_max_f(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));   // non-negative floats order as uints
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -927,6 +1019,35 @@ cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, i
   return cudaGetLastError();
 }
 
+cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
+                              cudaStream_t st) {
+  tc_recheck_kernel<<<148 * 4, 256, 0, st>>>(o.X, o.Bt, o.F, o.Fp, o.Cp, o.Dp, o.K, tc_kp(o.K), o.flags,
+                                             o.flag_count, o.flag_cap, shift, o.corr, o.dirty, o.recheck);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  tc_finalize_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, o.K, tc_kp(o.K), shift, S, o.corr,
+                                                                  o.dirty, labels, o.flag_count);
+  return cudaGetLastError();
+}
+
+int tc_corr_shift(const float* Cp, int64_t n, int64_t D) {
+  unsigned* d = nullptr;
+  unsigned h = 0;
+  if (cudaMalloc((void**)&d, sizeof(unsigned)) != cudaSuccess) return 0;
+  cudaMemset(d, 0, sizeof(unsigned));
+  absmax_kernel<<<148, 256>>>(Cp, n, d);
+  cudaMemcpy(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  float cmax;
+  memcpy(&cmax, &h, sizeof(float));
+  // |sum of corrections| <= 2 D max|C| 2^shift < 2^62
+  int ex = 0;
+  frexp((double)cmax * 2.0 * (double)(D > 0 ? D : 1), &ex);   // 2 D max|C| < 2^ex
+  int shift = 61 - ex;
+  if (shift > 900) shift = 900;
+  return shift;
+}
+
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st) {
   const int bn = tile_n_for(mode, o.K);
@@ -957,6 +1078,9 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.s_part_cap = o.s_part_slots;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
+  p.flags = o.flags;
+  p.flag_count = o.flag_count;
+  p.flag_cap = o.flag_cap;
   p.scores = scores;
   p.labels = labels;
   {

@@ -70,6 +70,13 @@ struct TcOperands {
   int64_t s_part_slots;
   unsigned* cnt;                     // [N_p / 128]
   unsigned long long* recheck;
+  // int8 mode deferred rechecks (tc_recheck_kernel / tc_finalize_kernel)
+  const float* Cp;                   // [K][Dp] fp32 class HVs (exact corrections)
+  uint2* flags;                      // [flag_cap] (row, d | provisional-negative << 31)
+  unsigned long long* flag_count;    // zero between calls
+  unsigned long long flag_cap;
+  long long* corr;                   // [N_p][Kp] fixed-point corrections, zero between calls
+  unsigned* dirty;                   // [N_p], zero between calls
 };
 int tc_tile_n(int mode, int64_t K);   // D-tile width of K4 (80 or 160)
 // Cluster shape of K4 for a mode (HDC_TC_CLUSTER="NxD" overrides, for measurements).
@@ -90,6 +97,11 @@ cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t ro
                             int64_t ld_src, int64_t Fp, void* out, cudaStream_t st);
 cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* scores, int32_t* labels,
                             int num_sms, cudaStream_t st);
+// int8 mode, after launch_fused_tc (which must have written S to `S`): float64 rechecks of
+// the listed signs, exact corrections of S and labels of the affected rows.
+cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
+                              cudaStream_t st);
+int tc_corr_shift(const float* Cp, int64_t n, int64_t D);   // fixed-point shift for |C| (synchronous)
 
 // K5: labels[r] = lowest-index argmax of S[r, 0:K).
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);

@@ -37,6 +37,10 @@ def main():
                 m.infer(X, path="fused")
                 ts.append(m.last_kernel_ms())
             ts = sorted(ts[2:])
+            if fl == 0:
+                n0 = m.recheck_count()
+                m.infer(X, path="fused")
+                print("  rechecks per launch: %d" % (m.recheck_count() - n0))
             print("%s %-8s cluster=%s debug=%-3d kernel_ms median %.4f min %.4f" % (cfg.name, prec, shape, fl, ts[len(ts) // 2], ts[0]), flush=True)
         os.environ["HDC_TC_DEBUG"] = "0"
         m.close()
