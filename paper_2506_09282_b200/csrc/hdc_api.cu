@@ -5,6 +5,7 @@
 // P:222): N <= 32 -> K2 small-batch D-split kernel; larger N ->
 // the fused large-batch kernel (FFMA fp32-exact or tcgen05 by precision).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -359,8 +360,12 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   m->tic(st);
   for (int64_t r0 = 0; r0 < N; r0 += chunk) {
     const int n = (int)((N - r0) < chunk ? (N - r0) : chunk);
-    cudaError_t e = launch_smallbatch(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
-                                      labels ? labels + r0 : nullptr, recheck, m->num_sms, st);
+    // K2s (TMA-streamed) when X fits its shared memory, else the register-strip K2
+    cudaError_t e = (m->B4 && smallstream_fits(m->F, m->D, m->K, n, m->num_sms) && !getenv("HDC_SMALL_LEGACY"))
+                        ? launch_smallstream(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
+                                             labels ? labels + r0 : nullptr, recheck, m->num_sms, st)
+                        : launch_smallbatch(mv, ws, X + r0 * m->F, n, scores ? scores + r0 * m->K : nullptr,
+                                            labels ? labels + r0 : nullptr, recheck, m->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "smallbatch launch");
     ++m->last_launches;
   }
@@ -427,7 +432,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   ALLOC(m->Cp, sizeof(float) * K * m->Dp);
   ALLOC(m->bnorm, sizeof(float) * m->Dp);
   ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
-  ALLOC(m->cnt, sizeof(unsigned) * 4);
+  ALLOC(m->cnt, sizeof(unsigned) * 64);
   ALLOC(m->recheck, sizeof(unsigned long long));
 #undef ALLOC
   if (e != cudaSuccess) {
@@ -444,7 +449,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = launch_unit_major(m->Bp, m->Fp, m->Dp, m->B4, st0);
   if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
-  if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 64);
   const int mode = tc_mode_of(m);
   const int64_t tn = tc_tile_n(mode < 0 ? 0 : mode, K);
   tc_cluster_shape(mode < 0 ? 0 : mode, K, &m->cl_n, &m->cl_d);

@@ -1,0 +1,478 @@
+// k_smallstream.cu -- K2s: HBM-streaming small-batch HDC inference (N <= 32).
+//
+// The whole of Alg. 1 for up to 32 rows of X in one launch:
+//   V = X B (fp32 FFMA), H = HardSign(V), S = H C^T,
+//   y = argmax_k S, lowest index on ties.
+// The work is bound by reading B (F x D fp32) once from HBM.  Partitioning is the
+// paper's ScalableHD-S (Alg. 3): D is split into one contiguous range of
+// 4-column units per CTA (148 CTAs); each CTA forms complete F-sums for its columns
+// (HardSign needs all of F), applies HardSign and contracts with its C columns into
+// a partial S (the paper's S_local); the partials are summed in a fixed order (the
+// paper's `S += S_local`) by a two-level last-arriver reduction.
+//
+// B200 mapping.  The model keeps B unit-major (B4[u][f][4]: all F rows of a 4-column
+// unit contiguous), so a CTA's share of B is one contiguous run of HBM.  A producer
+// warp streams it with 1-D TMA bulk copies (cp.async.bulk, 8 KB chunks) through a
+// shared-memory ring of up to 12 stages (96 KB in flight per SM: enough bytes in
+// flight to cover HBM latency at 1/148 of the chip's bandwidth), started before X is
+// staged; 8 consumer warps run the FFMA contraction from shared memory.
+//
+// HDC_PREC_FP32 sign exactness: |v| <= tau = c_F ||x_n|| ||b_d|| is re-evaluated in
+// float64 (warp-cooperative, fixed order), as in the other fp32 kernels.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace hdc {
+namespace {
+
+using namespace ptx;
+
+constexpr int kCw = 8;                         // consumer warps
+constexpr int kCt = 32 * kCw;                  // consumer threads
+constexpr int kThreadsS = kCt + 32;            // + producer warp (lane w feeds consumer warp w)
+constexpr int kChunkRows = 256;                // B4 rows per ring stage (4 KB)
+constexpr int kStagesMax = 8;                  // per consumer warp
+constexpr int kGroup = 8;                      // first-level reduction group (CTAs)
+
+struct StreamParams {
+  const float* X;
+  int nrows;
+  int64_t F, D, Dp, K, Fp;
+  const float* B4;       // [units][Fp][4]
+  const float* Cp;       // [K][Dp]
+  const float* bnorm;    // [Dp]
+  float tau_coef;
+  int recheck;
+  int G;                 // CTAs
+  int nst;               // ring stages per consumer warp
+  int max_cols;          // columns of the largest CTA range (4 ceil(units / G))
+  int64_t units;
+  float* S_part;         // [G + groups][NB][K]
+  unsigned* cnt;         // [1 + groups], zero between launches
+  unsigned long long* recheck_count;
+  float* scores;
+  int32_t* labels;
+  unsigned long long* dbg;   // diagnostics (HDC_SMALL_DEBUG): [0] min start, [1..7] max of phase ends (ns)
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SS_MARK(i)                                           \
+  do {                                                       \
+    if (p.dbg && (tid & 31) == 0) atomicMax(p.dbg + (i), gtime()); \
+  } while (0)
+
+__device__ __forceinline__ void cbar() {       // consumer warps only (named barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"n"(kCt) : "memory");
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamParams p) {
+  constexpr int NBP = (NB + 3) / 4 * 4;        // rows padded to float4
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int F = (int)p.F, K = (int)p.K, nst = p.nst;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);         // [kCw][kStagesMax]
+  uint64_t* empty = full + kCw * kStagesMax;
+  uint64_t* xfull = empty + kCw * kStagesMax;                 // X landed
+  float* ring = reinterpret_cast<float*>(smem + (2 * kCw * kStagesMax + 2) * 8);   // [kCw][nst][R][4]
+  // X rows as in global memory ([n][F], copied by one bulk copy from the 16-byte-aligned
+  // address at or below X; xoff floats of slack in front)
+  const uint64_t xaddr = reinterpret_cast<uint64_t>(p.X);
+  const int xoff = (int)((xaddr & 15u) >> 2);
+  const uint32_t xbytes = (uint32_t)(((xoff + p.nrows * F) * 4 + 15) & ~15);
+  float* Xraw = ring + (size_t)kCw * nst * kChunkRows * 4;     // [xbytes / 4]
+  const float* Xs = Xraw + xoff;                               // Xs[n * F + f]
+  auto up4 = [](size_t x) { return (x + 3) & ~size_t(3); };  // float4-aligned regions
+  float* Sw = Xraw + up4((size_t)NB * F + 4);                  // [kCw][NB][K] per-warp S_local
+  float* Cs = Sw + up4((size_t)kCw * NB * K);                  // [K][ncol] this CTA's C columns
+  float* bns = Cs + up4((size_t)K * p.max_cols);               // [ncol] ||b_d||
+  float* fin = bns + up4(p.max_cols);                          // [NB K + 32 + 4 kCt] final sums
+  __shared__ float xnorm_s[NBP];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = blockIdx.x;
+  const int64_t u0 = (int64_t)c * p.units / p.G, u1 = (int64_t)(c + 1) * p.units / p.G;
+  const int nch = (F + kChunkRows - 1) / kChunkRows;         // chunks per unit
+
+  if (p.dbg && tid == 0) atomicMin(p.dbg, gtime());
+  if (tid < kCw * nst) {
+    const int w = tid / nst, st = tid % nst;
+    mbar_init(full + w * kStagesMax + st, 1);
+    mbar_init(empty + w * kStagesMax + st, 1);
+  }
+  if (tid == 0) mbar_init(xfull, 1);
+  fence_mbar_init();
+  __syncthreads();
+
+  if (warp == kCw) {
+    // ===================================================== producer: lane w streams warp w's units
+    if (lane == kCw) {          // X, one bulk copy, issued first
+      mbar_arrive_expect_tx(xfull, xbytes);
+      bulk_load(Xraw, reinterpret_cast<const void*>(xaddr & ~uint64_t(15)), xbytes, xfull);
+    }
+    if (lane < kCw) {
+      const int w = lane;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t u = u0 + w; u < u1; u += kCw)
+        for (int ch = 0; ch < nch; ++ch) {
+          const int f0 = ch * kChunkRows, rows = min(kChunkRows, F - f0);
+          mbar_wait(empty + w * kStagesMax + st, ph ^ 1);
+          mbar_arrive_expect_tx(full + w * kStagesMax + st, (uint32_t)rows * 16u);
+          bulk_load(ring + ((size_t)w * nst + st) * kChunkRows * 4, p.B4 + (u * p.Fp + f0) * 4,
+                    (uint32_t)rows * 16u, full + w * kStagesMax + st);
+          if (++st == nst) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+    }
+    return;   // the producer takes no part in the rest (consumer barriers are named)
+  }
+
+  // ===================================================== consumers
+  // Stage X (nrows x F) -> Xs[f][n], this CTA's columns of C -> Cs[k][cols] and of ||b_d||
+  // -> bns, all loads of a batch issued before any store (one HBM latency per batch),
+  // while the producer's first chunks are already in flight.
+  const int ncol = (int)(u1 - u0) * 4;
+  const int64_t col0 = u0 * 4;
+  {
+    constexpr int BATCH = 8;
+    const int nc = K * ncol, total = nc + ncol;
+    for (int i0 = tid; i0 < total; i0 += kCt * BATCH) {
+      float v[BATCH];
+#pragma unroll
+      for (int j = 0; j < BATCH; ++j) {
+        const int i = i0 + j * kCt;
+        v[j] = 0.f;
+        if (i < nc) v[j] = __ldg(p.Cp + (int64_t)(i / ncol) * p.Dp + col0 + i % ncol);
+        else if (i < total) v[j] = __ldg(p.bnorm + col0 + (i - nc));
+      }
+#pragma unroll
+      for (int j = 0; j < BATCH; ++j) {
+        const int i = i0 + j * kCt;
+        if (i < nc) Cs[i] = v[j];
+        else if (i < total) bns[i - nc] = v[j];
+      }
+    }
+  }
+  float* sw = Sw + (size_t)warp * NB * K;
+  for (int i = lane; i < NB * K; i += 32) sw[i] = 0.f;
+  cbar();
+  mbar_wait(xfull, 0);
+  for (int n = warp; n < p.nrows; n += kCw) {
+    float ss = 0.f;
+    for (int f = lane; f < F; f += 32) ss = fmaf(Xs[n * F + f], Xs[n * F + f], ss);
+    ss = warp_sum_xor(ss);
+    if (lane == 0) xnorm_s[n] = sqrtf(ss);
+  }
+  cbar();
+  SS_MARK(1);
+
+  // (n, q) elements a lane owns after the cross-lane reduction: e = EPL lane + i
+  constexpr int NV = NB * 4;                          // V values of a unit
+  constexpr int EPL = NV >= 32 ? NV / 32 : 1;         // per lane (reduce-scatter), else lane e < NV
+  int st = 0;
+  uint32_t ph = 0;
+  unsigned long long nrecheck = 0;
+  for (int64_t u = u0 + warp; u < u1; u += kCw) {
+    // ---- V[n][0..3] for this unit, lanes over f (fp32 FMA, f ascending per lane)
+    float acc[NV];
+    float2 acc2[NV / 2];                          // packed (q0, q1), (q2, q3): FFMA2
+#pragma unroll
+    for (int e = 0; e < NV / 2; ++e) acc2[e] = make_float2(0.f, 0.f);
+    for (int ch = 0; ch < nch; ++ch) {
+      const int f0 = ch * kChunkRows, rows = min(kChunkRows, F - f0);
+      mbar_wait(full + warp * kStagesMax + st, ph);
+      const float4* b4 = reinterpret_cast<const float4*>(ring + ((size_t)warp * nst + st) * kChunkRows * 4);
+#pragma unroll 2
+      for (int r = lane; r < rows; r += 32) {
+        const float4 b = b4[r];
+        const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
+        const float* xc = Xs + f0 + r;                // column f of X: Xs[n F + f]
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const float x = n < p.nrows ? xc[n * F] : 0.f;
+          acc2[n * 2 + 0] = ffma2(x, b01, acc2[n * 2 + 0]);   // each lane: fmaf(x, b_q, acc)
+          acc2[n * 2 + 1] = ffma2(x, b23, acc2[n * 2 + 1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + warp * kStagesMax + st);
+      if (++st == nst) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < NV / 2; ++e) {
+      acc[2 * e] = acc2[e].x;
+      acc[2 * e + 1] = acc2[e].y;
+    }
+    // ---- complete the F-sums across lanes with a fixed pairwise tree
+    float vv[EPL];
+    if constexpr (NV >= 32) {
+      // reduce-scatter: at offset o a lane keeps the half of its values selected by lane bit o
+      // and adds the partner's copy of that half; after 5 steps lane l holds e = EPL l + i
+#pragma unroll
+      for (int o = 16, m = NV; o >= 1; o >>= 1, m >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < m / 2; ++i) {
+          const float keep = hi ? acc[i + m / 2] : acc[i];
+          const float send = hi ? acc[i] : acc[i + m / 2];
+          acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) vv[i] = acc[i];
+    } else {
+#pragma unroll
+      for (int e = 0; e < NV; ++e) acc[e] = warp_sum_xor(acc[e]);
+      vv[0] = 0.f;
+#pragma unroll
+      for (int e = 0; e < NV; ++e)
+        if (lane == e) vv[0] = acc[e];
+    }
+    float hh[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int e = (NV >= 32) ? EPL * lane + i : lane, n = e >> 2, q = e & 3;
+      const int64_t d = u * 4 + q;
+      bool flag = false;
+      if (p.recheck && e < NV && n < p.nrows && d < p.D) {
+        const float tau = p.tau_coef * xnorm_s[n] * bns[(int)(d - col0)] + kSignBoundAbs;
+        flag = fabsf(vv[i]) <= tau;
+      }
+      hh[i] = hardsign(vv[i]);
+      unsigned mask = __ballot_sync(0xffffffffu, flag);
+      nrecheck += __popc(mask);
+      while (mask) {            // float64 re-evaluation, fixed lane order
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int se = (NV >= 32) ? EPL * src + i : src, sn = se >> 2, sq = se & 3;
+        const float* bu = p.B4 + u * p.Fp * 4 + sq;
+        double a64 = 0.0;
+        for (int f = lane; f < F; f += 32) a64 = fma((double)Xs[sn * F + f], (double)__ldg(bu + f * 4), a64);
+        a64 = warp_sum_xor(a64);
+        if (lane == src) hh[i] = a64 >= 0.0 ? 1.f : -1.f;
+      }
+    }
+    // ---- S_local[n][k] += sum_q H[n][q] C[k][4u + q]  (q ascending; padded C = 0)
+    const int cl = (int)(u - u0) * 4;
+    for (int i0 = 0; i0 < p.nrows * K; i0 += 32) {  // warp-uniform trip count (shuffles)
+      const int i = i0 + lane;
+      const bool ok = i < p.nrows * K;
+      const int n = ok ? i / K : 0, k = ok ? i % K : 0;
+      float h[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = n * 4 + q;                      // owner: lane e / EPL, slot e % EPL
+        float hv = 0.f;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const float t = __shfl_sync(0xffffffffu, hh[j], (NV >= 32) ? (e / EPL) & 31 : e & 31);
+          if (((NV >= 32) ? e % EPL : 0) == j) hv = t;
+        }
+        h[q] = hv;
+      }
+      if (ok) {
+        const float* cr = Cs + k * ncol + cl;
+        float a = sw[i];
+        a = fmaf(h[0], cr[0], a);
+        a = fmaf(h[1], cr[1], a);
+        a = fmaf(h[2], cr[2], a);
+        a = fmaf(h[3], cr[3], a);
+        sw[i] = a;
+      }
+    }
+  }
+  if (lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
+  SS_MARK(2);
+  cbar();
+
+  // ---- CTA S_local = per-warp partials in warp order; the last-arriving CTA sums the
+  // G partials (all loads in flight at once) in a fixed order and takes the argmax
+  const int nk = p.nrows * K;
+  const int pst = (NB * K + 3) & ~3;               // partial stride (float4 aligned)
+  float* mypart = p.S_part + (int64_t)c * pst;
+  for (int i = tid; i < nk; i += kCt) {
+    float a = Sw[i];
+    for (int w = 1; w < kCw; ++w) a += Sw[(size_t)w * NB * K + i];
+    mypart[i] = a;
+  }
+  __threadfence();
+  cbar();
+  SS_MARK(3);
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(p.cnt, 1u);
+    s_last = (prev == (unsigned)(p.G - 1)) ? 1 : 0;
+    if (s_last) p.cnt[0] = 0u;
+  }
+  cbar();
+  if (!s_last) return;
+  __threadfence();
+  // thread layout: kCt threads = P partial-lanes x Q4 output quads; lane j sums partials
+  // j, j + P, ... in order (float4 loads, 8 in flight), then the P lane sums in a fixed order
+  float* Sfin = fin;                                  // [nk]
+  float4* tmp = reinterpret_cast<float4*>(fin + ((nk + 31) & ~31));   // [P][Q4]
+  const int nq = (nk + 3) / 4;
+  const int P = nq >= kCt ? 1 : (nq >= kCt / 2 ? 2 : (nq >= kCt / 4 ? 4 : (nq >= kCt / 8 ? 8 :
+                (nq >= kCt / 16 ? 16 : 32))));
+  const int Q4 = kCt / P;
+  for (int q0 = 0; q0 < nq; q0 += Q4) {
+    const int j = tid / Q4, q = q0 + tid % Q4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < nq) {
+      constexpr int BATCH = 8;
+      for (int cc0 = j; cc0 < p.G; cc0 += P * BATCH) {
+        float4 v[BATCH];
+#pragma unroll
+        for (int b = 0; b < BATCH; ++b) {
+          const int cc = cc0 + b * P;
+          v[b] = cc < p.G ? __ldcg(reinterpret_cast<const float4*>(p.S_part + (int64_t)cc * pst) + q)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int b = 0; b < BATCH; ++b)
+          if (cc0 + b * P < p.G) {
+            if (cc0 == j && b == 0) a = v[b];
+            else {
+              a.x += v[b].x;
+              a.y += v[b].y;
+              a.z += v[b].z;
+              a.w += v[b].w;
+            }
+          }
+      }
+      tmp[j * Q4 + (q - q0)] = a;
+    }
+    cbar();
+    if (tid < Q4 && q0 + tid < nq) {
+      float4 t = tmp[tid];
+      for (int jj = 1; jj < P; ++jj) {
+        const float4 u = tmp[jj * Q4 + tid];
+        t.x += u.x;
+        t.y += u.y;
+        t.z += u.z;
+        t.w += u.w;
+      }
+      const float tv[4] = {t.x, t.y, t.z, t.w};
+      for (int i = 0; i < 4; ++i) {
+        const int e = 4 * (q0 + tid) + i;
+        if (e < nk) {
+          Sfin[e] = tv[i];
+          if (p.scores) p.scores[e] = tv[i];
+        }
+      }
+    }
+    cbar();
+  }
+  SS_MARK(4);
+  if (p.labels)
+    for (int n = tid; n < p.nrows; n += kCt) {
+      int best = 0;
+      float bv = Sfin[n * K];
+      for (int k = 1; k < K; ++k)
+        if (Sfin[n * K + k] > bv) {
+          bv = Sfin[n * K + k];
+          best = k;
+        }
+      p.labels[n] = best;
+    }
+}
+
+size_t stream_smem(int nst, int64_t F, int NB, int64_t K, int64_t max_cols) {
+  return (2 * kCw * kStagesMax + 2) * 8 +
+         sizeof(float) * ((size_t)kCw * nst * kChunkRows * 4 + (size_t)F * NB + 8 + (size_t)kCw * NB * K +
+                          (size_t)(K + 1) * max_cols + (size_t)NB * K + 32 + 4 * kCt + 32);
+}
+
+template <int NB>
+cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
+  const size_t lim = 225 * 1024;
+  int nst = kStagesMax;
+  while (nst > 2 && stream_smem(nst, p.F, NB, p.K, p.max_cols) > lim) --nst;
+  const size_t sm = stream_smem(nst, p.F, NB, p.K, p.max_cols);
+  if (sm > lim) return cudaErrorInvalidValue;
+  p.nst = nst;
+  static size_t attr_set = 0;                   // host-side attribute call only when it grows
+  if (sm > attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(smallstream_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lim);
+    if (e != cudaSuccess) return e;
+    attr_set = lim;
+  }
+  static unsigned long long* dbg = nullptr;
+  const bool debug = getenv("HDC_SMALL_DEBUG") != nullptr;
+  if (debug) {
+    if (!dbg) cudaMalloc((void**)&dbg, 8 * sizeof(unsigned long long));
+    unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    p.dbg = dbg;
+  }
+  smallstream_kernel<NB><<<p.G, kThreadsS, sm, st>>>(p);
+  cudaError_t le = cudaGetLastError();
+  if (debug && le == cudaSuccess) {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[hdc smallstream debug] NB=%d nst=%d: from first CTA start (us): X staged %.2f, "
+            "stream done %.2f, published %.2f, final %.2f\n", NB, p.nst, (h[1] - h[0]) * 1e-3,
+            (h[2] - h[0]) * 1e-3, (h[3] - h[0]) * 1e-3, h[4] ? (h[4] - h[0]) * 1e-3 : -1.0);
+  }
+  return le;
+}
+
+}  // namespace
+
+bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms) {
+  const int nb = n <= 1 ? 1 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : 32;   // template NB used
+  const int64_t units = (D + 3) / 4, G = std::min<int64_t>(units, num_sms);
+  return stream_smem(2, F, nb, K, 4 * ((units + G - 1) / G)) <= 225 * 1024 &&
+         (int64_t)n * F * 4 + 16 < (int64_t(1) << 20);          // one bulk copy (tx-count limit)
+}
+
+cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, const float* X, int n,
+                               float* scores, int32_t* labels, bool recheck, int num_sms,
+                               cudaStream_t st) {
+  StreamParams p;
+  p.X = X;
+  p.nrows = n;
+  p.F = m.F;
+  p.D = m.D;
+  p.Dp = m.Dp;
+  p.K = m.K;
+  p.Fp = m.Fp;
+  p.B4 = m.B4;
+  p.Cp = m.Cp;
+  p.bnorm = m.bnorm;
+  p.tau_coef = m.tau_coef;
+  p.recheck = recheck ? 1 : 0;
+  p.units = (m.D + 3) / 4;
+  p.G = (int)std::min<int64_t>(p.units, num_sms);
+  p.max_cols = (int)(4 * ((p.units + p.G - 1) / p.G));
+  p.nst = 0;
+  p.S_part = ws.S_part;
+  p.cnt = ws.cnt1;
+  p.recheck_count = ws.recheck;
+  p.scores = scores;
+  p.labels = labels;
+  p.dbg = nullptr;
+  if (n <= 1) return launch_stream_nb<1>(p, st);
+  if (n <= 4) return launch_stream_nb<4>(p, st);
+  if (n <= 8) return launch_stream_nb<8>(p, st);
+  if (n <= 16) return launch_stream_nb<16>(p, st);
+  return launch_stream_nb<32>(p, st);
+}
+
+}  // namespace hdc

@@ -25,7 +25,7 @@ constexpr int64_t kFPad = 64;   // F padding granule (covers every kernel's K st
 // Workspace for the small-batch kernel's cross-CTA reduction.
 struct SmallWorkspace {
   float* S_part;         // [num_sms][32][K]
-  unsigned* cnt1;        // [1], zero between launches
+  unsigned* cnt1;        // [64] last-arriver counters, zero between launches
   unsigned long long* recheck;  // fp64 re-evaluation counter (diagnostic)
 };
 
@@ -37,6 +37,12 @@ int small_max_rows(int64_t F, int64_t D, int64_t K, int num_sms);     // rows pe
 cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, const float* X,
                               int n, float* scores, int32_t* labels, bool recheck, int num_sms,
                               cudaStream_t st);
+
+// K2s (k_smallstream.cu): TMA-streamed small-batch kernel, rows [0, n), n <= 32.
+bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms);
+cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, const float* X, int n,
+                               float* scores, int32_t* labels, bool recheck, int num_sms,
+                               cudaStream_t st);
 
 // Workspace of the fused large-batch kernels (grown with N).
 struct FusedWorkspace {
