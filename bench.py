@@ -142,6 +142,24 @@ def cpu_model():
     return "unknown"
 
 
+def measured_traffic(cfg_name, prec):
+    """DRAM bytes per launch of the dominant kernel from the newest committed ncu
+    --set full capture (profiles/**/traffic.json), else None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "**", "traffic.json"), recursive=True),
+                    key=os.path.getmtime):
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+            e = d.get("%s/%s" % (cfg_name, prec))
+            if e:
+                best = e.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    return best
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
     from hdc_inputs import CONFIGS, make_B, make_C, make_X
@@ -321,6 +339,9 @@ def run_ours(args, rank, world, local_rank):
         return
     roof = roofline_for(cfg, args.prec, args.path, kernel_ms, peaks, clk["sm_mhz"])
     roof["peak_source"] = peaks_src
+    roof["traffic"] = measured_traffic(cfg.name, args.prec)
+    if roof["traffic"] is not None:
+        roof["traffic_source"] = "ncu --set full dram bytes per launch (profiles/**/traffic.json)"
     roof["kernel_ms"] = kernel_ms
     roof["kernel_share_of_step"] = kernel_ms / ms_per_step
     cpu = None

@@ -107,9 +107,14 @@ hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int3
                                   float* scores, hdc_path_t path, void* stream);
 
 /* End-to-end variant on HOST buffers: copies X_host (N*F fp32) to the device,
- * runs hdc_model_infer, copies labels (and scores if non-NULL) back.  Host
- * buffers should be pinned (cudaHostAlloc) for the copies to be asynchronous;
- * the call returns after enqueue -- synchronise `stream` before reading them. */
+ * runs hdc_model_infer, copies labels (and scores if non-NULL) back.  For N > 32
+ * the rows are processed in up to 8 chunks of ~4096 whose host-to-device copies
+ * run on a library-owned copy stream, overlapping the inference of the previous
+ * chunk (rows are independent, so results equal the one-shot call).
+ * Host buffers should be pinned (cudaHostAlloc) for the copies to be
+ * asynchronous; the call returns after enqueue -- synchronise `stream` before
+ * reading them.  Concurrent host-path calls on the same model must be serialised
+ * by the caller (they share the model's staging buffers and copy stream). */
 hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                                   int32_t* labels_host, float* scores_host, void* stream);
 

@@ -40,6 +40,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr int64_t kMaxF = int64_t(1) << 20;
 constexpr int kSmallMaxN = 32;
+constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 
 }  // namespace
 
@@ -90,6 +91,9 @@ struct hdc_model_s {
   int64_t Xdev_rows = 0;
   int32_t* ldev = nullptr;
   float* sdev = nullptr;
+  cudaStream_t copy_stream = nullptr;   // host-buffer path: H2D copies, overlapped with compute
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_h2d[8] = {};
   int32_t last_launches = 0;
   // diagnostics: CUDA events around the dominant kernel of each call
   bool timing = false;
@@ -132,6 +136,10 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 }
 
 void free_model_memory(hdc_model_s* m) {
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->ev_start) cudaEventDestroy(m->ev_start);
+  for (int i = 0; i < kHostChunksMax; ++i)
+    if (m->ev_h2d[i]) cudaEventDestroy(m->ev_h2d[i]);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   cudaFree(m->Btc);
@@ -549,16 +557,47 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
     }
     m->Xdev_rows = N;
   }
-  HDC_CUDA_TRY(cudaMemcpyAsync(m->Xdev, X_host, sizeof(float) * N * m->F, cudaMemcpyHostToDevice, s),
-               "H2D X");
-  st = run(m, m->Xdev, N, m->ldev, scores_host ? m->sdev : nullptr, HDC_PATH_AUTO, s);
-  if (st != HDC_OK) return st;
-  HDC_CUDA_TRY(cudaMemcpyAsync(labels_host, m->ldev, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s),
-               "D2H labels");
-  if (scores_host)
-    HDC_CUDA_TRY(cudaMemcpyAsync(scores_host, m->sdev, sizeof(float) * N * m->K,
-                                 cudaMemcpyDeviceToHost, s),
-                 "D2H scores");
+  if (!m->copy_stream) {
+    if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming) != cudaSuccess)
+      return fail(HDC_ERR_CUDA, "copy stream / event creation");
+    for (int i = 0; i < kHostChunksMax; ++i)
+      if (cudaEventCreateWithFlags(&m->ev_h2d[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(HDC_ERR_CUDA, "event creation");
+  }
+  // Pipelined: the H2D copy of chunk i + 1 (copy stream) overlaps the inference of chunk i
+  // (caller's stream); labels (and scores) come back per chunk.  Rows are independent
+  // (Alg. 1 per sample), so chunking changes nothing in the results.
+  int nchunks = 1;
+  if (N > kSmallMaxN) {
+    const int64_t target = 4096;                      // rows per chunk (>= one full wave of tiles)
+    nchunks = (int)((N + target - 1) / target);
+    if (nchunks > kHostChunksMax) nchunks = kHostChunksMax;
+  }
+  const int64_t per = (N + nchunks - 1) / nchunks;
+  HDC_CUDA_TRY(cudaEventRecord(m->ev_start, s), "event record");
+  HDC_CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->ev_start, 0), "stream wait");
+  int32_t launches = 0;
+  for (int i = 0; i < nchunks; ++i) {
+    const int64_t r0 = i * per, n = (r0 + per <= N) ? per : N - r0;
+    if (n <= 0) break;
+    HDC_CUDA_TRY(cudaMemcpyAsync(m->Xdev + r0 * m->F, X_host + r0 * m->F, sizeof(float) * n * m->F,
+                                 cudaMemcpyHostToDevice, m->copy_stream),
+                 "H2D X");
+    HDC_CUDA_TRY(cudaEventRecord(m->ev_h2d[i], m->copy_stream), "event record");
+    HDC_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_h2d[i], 0), "stream wait");
+    st = run(m, m->Xdev + r0 * m->F, n, m->ldev + r0, scores_host ? m->sdev + r0 * m->K : nullptr,
+             HDC_PATH_AUTO, s);
+    if (st != HDC_OK) return st;
+    launches += m->last_launches;
+    HDC_CUDA_TRY(cudaMemcpyAsync(labels_host + r0, m->ldev + r0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s),
+                 "D2H labels");
+    if (scores_host)
+      HDC_CUDA_TRY(cudaMemcpyAsync(scores_host + r0 * m->K, m->sdev + r0 * m->K, sizeof(float) * n * m->K,
+                                   cudaMemcpyDeviceToHost, s),
+                   "D2H scores");
+  }
+  m->last_launches = launches;
   return HDC_OK;
 }
 
