@@ -95,6 +95,7 @@ hdc_status_t hdc_infer(const float* X, const float* B, const float* C, int64_t N
  * layouts and precomputes per-column norms ||b_d|| (sign recheck) and any
  * low-precision operand copies `prec` needs.  Timed latency excludes this, as
  * the paper's pre-tiled B and J.  Synchronises the device. */
+/* (C may be NULL: encoder-only model for hdc_model_encode; K still sets the class count.) */
 hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t D, int64_t K,
                               hdc_precision_t prec, hdc_model_t* out);
 
@@ -127,6 +128,35 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
 
 /* Row argmax, lowest index among equal maxima: labels[n] = argmax_k S[n*K+k]. */
 hdc_status_t hdc_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, void* stream);
+
+/* ---- Materialised H: encoding, unfused similarity (ablation), single-pass training ----
+ * Bit-packed layout of H (N x D signs): row n, column d at word H[n*ldw + d/32],
+ * bit d%32; the bit is SET iff h[n,d] = -1 (HardSign).  ldw >= ceil(D/32).
+ *
+ * Stage I alone, H = HardSign(X B) (eq. batch_encode), written to
+ * H [N*ldw] (device, caller-owned, cleared by the call).  The model must use a
+ * tensor-core precision; HDC_PREC_FP32_TC gives the exact signs of the fp32 product
+ * (float64 re-evaluation of the bound-flagged ones).  A model created
+ * with C == NULL is an encoder-only model (hdc_model_infer rejects it).
+ * Errors: INVALID_VALUE (null pointers, ldw too small), UNSUPPORTED (FP32 FFMA model,
+ * N >= 2^31), MISALIGNED (4-byte alignment). */
+hdc_status_t hdc_model_encode(hdc_model_t m, const float* X, int64_t N, uint32_t* H, int64_t ldw,
+                              void* stream);
+
+/* Stage II + argmax from a packed H (the unfused variant of Alg. 1 used to measure
+ * what fusion saves): S[n,k] = sum_d h[n,d] C[k,d] (d ascending,
+ * fp32), labels = lowest-index argmax.  C [K*D] fp32 device; labels [N] and/or
+ * scores [N*K] (either may be NULL, not both).  K <= 64. */
+hdc_status_t hdc_similarity_packed(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,
+                                   int64_t K, int32_t* labels, float* scores, void* stream);
+
+/* Single-pass training (constrained bundling P:94-105): for labels y [N] in
+ * [0, K), counts[k*D+d] += sum_{n: y_n = k} h[n,d] (int32, exact, accumulates: clear it
+ * first), and if M != NULL the class HVs M[k*D+d] = HardSign(counts) = +1 / -1 (fp32,
+ * ties +1).  Synchronises `stream` to validate the labels (INVALID_VALUE if any is out
+ * of range). */
+hdc_status_t hdc_bundle_classes(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const int32_t* y,
+                                int64_t K, int32_t* counts, float* M, void* stream);
 
 /* Releases the model and its device memory.  Synchronises the device. */
 hdc_status_t hdc_model_destroy(hdc_model_t m);

@@ -44,6 +44,10 @@ def _load():
         lib.oracle_hardsign.argtypes = [ctypes.c_double]
         lib.oracle_hardsign.restype = ctypes.c_double
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_encode.argtypes = [P, P, I64, I64, I64, P]
+        lib.oracle_encode.restype = ctypes.c_int
+        lib.oracle_train.argtypes = [P, P, I64, I64, I64, P, P]
+        lib.oracle_train.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -117,3 +121,31 @@ def infer(X, B, C, allow=False, nthreads=1):
     out["rowscale"] = np.max(np.abs(S), axis=1) if N else np.zeros(0)
     out["c1"] = np.sum(np.abs(C.astype(np.float64)), axis=1)
     return out
+
+
+def encode(X, B):
+    """H = HardSign(X B) as int8 +-1 (eq. batch_encode, HardSign P:126-131)."""
+    X, B = _f32(X), _f32(B)
+    N, F = X.shape
+    F2, D = B.shape
+    if F != F2:
+        raise OracleError("dimension mismatch")
+    H = np.empty((N, D), dtype=np.int8)
+    rc = _load().oracle_encode(_ptr(X), _ptr(B), N, F, D, _ptr(H))
+    if rc:
+        raise OracleError("non-finite input" if rc == 1 else "oracle error %d" % rc)
+    return H
+
+
+def train(H, y, K):
+    """Single-pass training: counts[k] = sum of H rows of class k (int64),
+    M = HardSign(counts) (float64 +-1, ties +1)."""
+    H = np.ascontiguousarray(H, dtype=np.int8)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    N, D = H.shape
+    counts = np.empty((K, D), dtype=np.int64)
+    M = np.empty((K, D), dtype=np.float64)
+    rc = _load().oracle_train(_ptr(H), _ptr(y), N, D, K, _ptr(counts), _ptr(M))
+    if rc:
+        raise OracleError("label outside [0, K)" if rc == 3 else "oracle error %d" % rc)
+    return counts, M

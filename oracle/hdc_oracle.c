@@ -134,3 +134,40 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Encoding alone, H = HardSign(X B) (eq. batch_encode P:173-176 with the HardSign
+ * activation P:126-131), as int8 +1 / -1, rows [0,N).  Same float64 sum as
+ * oracle_preact (f ascending). */
+int oracle_encode(const float* X, const float* B, int64_t N, int64_t F, int64_t D, int8_t* H) {
+  if (!all_finite(X, N * F) || !all_finite(B, F * D)) return 1;
+  double* v = (double*)malloc(sizeof(double) * (D > 0 ? D : 1));
+  if (!v) return 2;
+  for (int64_t n = 0; n < N; ++n) {
+    for (int64_t d = 0; d < D; ++d) v[d] = 0.0;
+    for (int64_t f = 0; f < F; ++f) {
+      const double x = (double)X[n * F + f];
+      const float* b = B + f * D;
+      for (int64_t d = 0; d < D; ++d) v[d] += x * (double)b[d];
+    }
+    for (int64_t d = 0; d < D; ++d) H[n * D + d] = (int8_t)oracle_hardsign(v[d]);
+  }
+  free(v);
+  return 0;
+}
+
+/* Single-pass training: the class codebook by constrained bundling of the
+ * encoded HVs of each class.  Bundling is element-wise addition, so
+ *   counts[k,d] = sum_{n : y[n] = k} H[n,d]        (exact integers)
+ * and the normalised class HV is M[k,d] = HardSign(counts[k,d]) (a tie,
+ * count 0, gives +1).  Labels outside [0,K) return 3. */
+int oracle_train(const int8_t* H, const int32_t* y, int64_t N, int64_t D, int64_t K, int64_t* counts,
+                 double* M) {
+  for (int64_t i = 0; i < K * D; ++i) counts[i] = 0;
+  for (int64_t n = 0; n < N; ++n) {
+    if (y[n] < 0 || y[n] >= K) return 3;
+    for (int64_t d = 0; d < D; ++d) counts[(int64_t)y[n] * D + d] += H[n * D + d];
+  }
+  if (M)
+    for (int64_t i = 0; i < K * D; ++i) M[i] = oracle_hardsign((double)counts[i]);
+  return 0;
+}

@@ -63,12 +63,15 @@ struct hdc_model_s {
   int64_t tw_slots = 0;      // capacity of S_part_tc in [128][K] slots
   // int8 mode deferred rechecks: listed signs, fixed-point corrections, affected rows
   int corr_shift = 0;
+  bool has_c = true;         // false: encoder-only model (created with C == NULL)
   uint2* flags = nullptr;
   unsigned long long* flag_count = nullptr;
   unsigned long long flag_cap = 0;
   long long* corr = nullptr;          // [tw_rows][Kp]
   unsigned* dirty = nullptr;          // [tw_rows]
   float* S_ws = nullptr;              // [tw_rows][K] scores when the caller passes none
+  uint32_t* hout = nullptr;           // set only during hdc_model_encode
+  int64_t hout_ldw = 0;
   void* Atc = nullptr;       // [NL][Np][Fp]
   int64_t* rowtau = nullptr; // [Np]
   float* S_part_tc = nullptr;
@@ -313,6 +316,8 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.flag_cap = m->flag_cap;
   o.corr = m->corr;
   o.dirty = m->dirty;
+  o.hout = m->hout;
+  o.hout_ldw = m->hout_ldw;
   // int8 mode: the fused kernel always writes (provisional) scores, corrected afterwards
   float* S = (mode == 2 && !scores) ? m->S_ws : scores;
   m->tic(st);
@@ -384,6 +389,7 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
 hdc_status_t validate_call(hdc_model_s* m, const float* X, int64_t N, const void* out_required,
                            const void* out_optional) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  if (!m->has_c) return fail(HDC_ERR_INVALID_VALUE, "encoder-only model (created without C)");
   if (N < 0) return fail(HDC_ERR_INVALID_VALUE, "N < 0");
   if (N >= (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "N >= 2^31 (row indices are 32-bit)");
   if (N > 0 && (!X || !out_required)) return fail(HDC_ERR_INVALID_VALUE, "null X or output");
@@ -418,7 +424,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   *out = nullptr;
   hdc_status_t st = check_dims(F, D, K);
   if (st != HDC_OK) return st;
-  if (!B || !C) return fail(HDC_ERR_INVALID_VALUE, "null B or C");
+  if (!B) return fail(HDC_ERR_INVALID_VALUE, "null B");
   if (!aligned(B, 4) || !aligned(C, 4)) return fail(HDC_ERR_MISALIGNED, "B, C must be 4-byte aligned");
   if (prec < HDC_PREC_FP32 || prec > HDC_PREC_FP32_TC) return fail(HDC_ERR_INVALID_VALUE, "bad precision");
   hdc_model_s* m = new hdc_model_s();
@@ -455,7 +461,9 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = launch_pad_copy(B, F, D, m->Bp, m->Dp, st0);
   if (e == cudaSuccess) e = launch_transpose(m->Bp, m->Fp, m->Dp, m->Bt, st0);
   if (e == cudaSuccess) e = launch_unit_major(m->Bp, m->Fp, m->Dp, m->B4, st0);
-  if (e == cudaSuccess) e = launch_pad_copy(C, K, D, m->Cp, m->Dp, st0);
+  m->has_c = C != nullptr;
+  if (e == cudaSuccess) e = C ? launch_pad_copy(C, K, D, m->Cp, m->Dp, st0)
+                              : cudaMemset(m->Cp, 0, sizeof(float) * K * m->Dp);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 64);
   const int mode = tc_mode_of(m);
@@ -598,6 +606,66 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                    "D2H scores");
   }
   m->last_launches = launches;
+  return HDC_OK;
+}
+
+hdc_status_t hdc_model_encode(hdc_model_t m, const float* X, int64_t N, uint32_t* H, int64_t ldw,
+                              void* stream) {
+  if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  if (N < 0) return fail(HDC_ERR_INVALID_VALUE, "N < 0");
+  if (N >= (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "N >= 2^31");
+  if (N > 0 && (!X || !H)) return fail(HDC_ERR_INVALID_VALUE, "null X or H");
+  if (ldw < (m->D + 31) / 32) return fail(HDC_ERR_INVALID_VALUE, "ldw < ceil(D / 32)");
+  if (!aligned(X, 4) || !aligned(H, 4)) return fail(HDC_ERR_MISALIGNED, "pointers must be 4-byte aligned");
+  const int mode = tc_mode_of(m);
+  if (mode < 0 || !m->Btc)
+    return fail(HDC_ERR_UNSUPPORTED, "encode needs a tensor-core precision model (fp32_tc, tf32, bf16)");
+  if (N == 0) return HDC_OK;
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
+  cudaStream_t st = (cudaStream_t)stream;
+  HDC_CUDA_TRY(cudaMemsetAsync(H, 0, sizeof(uint32_t) * N * ldw, st), "H clear");
+  m->hout = H;
+  m->hout_ldw = ldw;
+  hdc_status_t s2 = run_fused_tc(m, X, N, nullptr, nullptr, st);
+  m->hout = nullptr;
+  m->hout_ldw = 0;
+  return s2;
+}
+
+hdc_status_t hdc_similarity_packed(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,
+                                   int64_t K, int32_t* labels, float* scores, void* stream) {
+  if (N < 0 || D < 1 || K < 1) return fail(HDC_ERR_INVALID_VALUE, "N >= 0, D >= 1, K >= 1 required");
+  if (K > 64) return fail(HDC_ERR_UNSUPPORTED, "K > 64 (unfused ablation kernel)");
+  if (ldw < (D + 31) / 32) return fail(HDC_ERR_INVALID_VALUE, "ldw < ceil(D / 32)");
+  if (N > 0 && (!H || !C || (!labels && !scores))) return fail(HDC_ERR_INVALID_VALUE, "null pointer");
+  if (!aligned(H, 4) || !aligned(C, 4) || !aligned(labels, 4) || !aligned(scores, 4))
+    return fail(HDC_ERR_MISALIGNED, "alignment");
+  if (N == 0) return HDC_OK;
+  cudaError_t e = launch_packed_similarity(H, ldw, N, D, C, K, labels, scores, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "packed similarity launch");
+  return HDC_OK;
+}
+
+hdc_status_t hdc_bundle_classes(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const int32_t* y,
+                                int64_t K, int32_t* counts, float* M, void* stream) {
+  if (N < 0 || D < 1 || K < 1) return fail(HDC_ERR_INVALID_VALUE, "N >= 0, D >= 1, K >= 1 required");
+  if (K > HDC_MAX_K) return fail(HDC_ERR_INVALID_VALUE, "K > HDC_MAX_K");
+  if (ldw < (D + 31) / 32) return fail(HDC_ERR_INVALID_VALUE, "ldw < ceil(D / 32)");
+  if (!counts || (N > 0 && (!H || !y))) return fail(HDC_ERR_INVALID_VALUE, "null pointer");
+  if (!aligned(H, 4) || !aligned(y, 4) || !aligned(counts, 4) || !aligned(M, 4))
+    return fail(HDC_ERR_MISALIGNED, "alignment");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned* err = nullptr;
+  HDC_CUDA_TRY(cudaMallocAsync((void**)&err, sizeof(unsigned), st), "workspace");
+  HDC_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned), st), "workspace");
+  cudaError_t e = launch_bundle(H, ldw, N, D, y, K, counts, M, err, st);
+  unsigned herr = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);      // label validation needs the count
+  cudaFreeAsync(err, st);
+  if (e != cudaSuccess) return cuda_fail(e, "bundle");
+  if (herr) return fail(HDC_ERR_INVALID_VALUE, "labels outside [0, K)");
   return HDC_OK;
 }
 

@@ -136,6 +136,8 @@ struct TcParams {
                            // else one per N-group of the cluster's range
   unsigned* cnt;           // [Tn]
   unsigned long long* recheck_count;
+  uint32_t* hout;                   // encode mode (hdc_model_encode): bit-packed H, bit set <=> h = -1;
+  int64_t hout_ldw;                 //   row n, column d at word n * ldw + d / 32, bit d % 32; no Stage II
   uint2* flags;                     // int8 mode: (row, d | provisional-negative << 31) to re-evaluate
   unsigned long long* flag_count;   // appended entries (may exceed flag_cap: overflow re-evaluated inline)
   unsigned long long flag_cap;
@@ -322,24 +324,6 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
     }
-  } else if (warp == 2) {
-    // ===================================================== C-tile producer (Stage II B operand)
-    // A separate warp, so the operand stream never waits for a C slot.
-    if (lane == 0) {
-      int cs = 0;
-      uint32_t cphase = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        const int di = (int)(t % p.TdG) * CLD + rd;
-        mbar_wait(cempty + cs, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));   // + taus
-        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
-        if constexpr (MODE == 2)
-          bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
-                    cfull + cs);
-        cs ^= 1;
-        if (cs == 0) cphase ^= 1;
-      }
-    }
   } else if (warp == 1) {
     // ===================================================== Stage I MMA issuer (elected lane)
     int stage = 0, buf = 0;
@@ -385,7 +369,28 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
     }
+  } else if (warp == 2) {
+    if (!p.hout) {   // encode mode: no Stage II, no C tiles
+    // ===================================================== C-tile producer (Stage II B operand)
+    // A separate warp, so the operand stream never waits for a C slot.
+    if (lane == 0) {
+      int cs = 0;
+      uint32_t cphase = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        const int di = (int)(t % p.TdG) * CLD + rd;
+        mbar_wait(cempty + cs, cphase ^ 1);
+        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));   // + taus
+        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
+        if constexpr (MODE == 2)
+          bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
+                    cfull + cs);
+        cs ^= 1;
+        if (cs == 0) cphase ^= 1;
+      }
+    }
+    }
   } else if (warp == 3) {
+    if (!p.hout) {
     // ===================================================== Stage II MMA issuer (elected lane)
     // A warp of its own: S += H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
     // never waiting behind (or holding up) the Stage I issue loop.
@@ -434,6 +439,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       cs ^= 1;
       if (cs == 0) cphase ^= 1;
     }
+    }
   } else if (warp >= EPI_WARP0) {
     // ===================================================== epilogue
     const int ew = warp - EPI_WARP0;
@@ -459,8 +465,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       TWAIT(6, tfull + buf, bphase);
       const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
       if constexpr (MODE == 2) {
-        TWAIT(15, cfull + cs, cphase);
-        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
+        if (p.hout) {
+          sct = p.coltau + (int64_t)di * BN;   // encode mode: no C tiles; taus from global
+        } else {
+          TWAIT(15, cfull + cs, cphase);
+          sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
+        }
       }
       tc_fence_after();
       // ---- phase 1: accumulator -> HardSign bits (bit set -> h = -1) and recheck flags
@@ -507,9 +517,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);   // accumulator free for tile t + 2
-      // H buffer hb free (Stage II of tile t - 2 done; its recheck queue drained)
-      TWAIT(7, hempty + hb, hphase ^ 1);
-      tc_fence_after();
+      // H buffer hb free (Stage II of tile t - 2 done)
+      if (!p.hout) {
+        TWAIT(7, hempty + hb, hphase ^ 1);
+        tc_fence_after();
+      }
       // ---- phase 2 (int8 mode): flagged signs are appended to a global list with the
       // provisional sign used in H; hdc_recheck_kernel re-evaluates them in float64 after
       // this kernel and corrects S exactly where a sign flips (Stage II is linear in H).
@@ -547,7 +559,24 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
       // ---- phase 3: H (exact bf16 +-1: 0x3F80 / 0xBF80) for the Stage II MMA
-      if (p.debug & 128) {
+      if (p.hout) {
+        // encode mode: OR this thread's sign bits into the packed rows (column groups of
+        // neighbouring threads / tiles share words; OR of disjoint bits is order-free)
+        if (row_ok) {
+          uint32_t* hr = p.hout + row * p.hout_ldw;
+          const int64_t g0 = (int64_t)di * BN + cq * EPI_COLS;
+#pragma unroll
+          for (int w = 0; w < NWB; ++w) {
+            const int nb = (EPI_COLS - 32 * w) < 32 ? (EPI_COLS - 32 * w) : 32;
+            const uint32_t bits = hbits[w] & (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u));
+            if (!bits) continue;
+            const int64_t gb = g0 + 32 * w, wi = gb >> 5;
+            const int sh = (int)(gb & 31);
+            if (wi < p.hout_ldw) atomicOr(hr + wi, bits << sh);
+            if (sh && wi + 1 < p.hout_ldw && (bits >> (32 - sh))) atomicOr(hr + wi + 1, bits >> (32 - sh));
+          }
+        }
+      } else if (p.debug & 128) {
         // diagnostics: no H write
       } else if constexpr (CF::H_TMEM) {
         // packed bf16 pairs into TMEM columns H_COL + col / 2 of this thread's lane
@@ -597,7 +626,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(hfull + hb);
+      if (lane == 0 && !p.hout) mbar_arrive(hfull + hb);
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
       if (++hb == NH) {
@@ -607,7 +636,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       cs ^= 1;
       if (cs == 0) cphase ^= 1;
 
-      if (!seg_last(t, t1, p.TdG)) continue;
+      if (p.hout || !seg_last(t, t1, p.TdG)) continue;
       // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM.  The
       // N-tile's D-groups are split over clusters c_first..c_last, each over its CLD ranks.
       const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G);
@@ -808,7 +837,8 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, const float* __re
                                   int64_t Kp, const uint2* __restrict__ flags,
                                   const unsigned long long* __restrict__ flag_count,
                                   unsigned long long cap, int shift, long long* __restrict__ corr,
-                                  unsigned* __restrict__ dirty, unsigned long long* recheck_count) {
+                                  unsigned* __restrict__ dirty, unsigned long long* recheck_count,
+                                  uint32_t* __restrict__ hout, int64_t hout_ldw) {
   const int lane = threadIdx.x & 31;
   const unsigned long long cnt = *flag_count;
   const unsigned long long n = cnt < cap ? cnt : cap;
@@ -820,7 +850,9 @@ __global__ void tc_recheck_kernel(const float* __restrict__ X, const float* __re
     const int64_t row = e.x, d = e.y & 0x7FFFFFFFu;
     const bool neg_prov = (e.y >> 31) != 0u;
     const float hv = recheck_dot(X + row * F, Bt + d * Fp, F, lane);
-    if ((hv < 0.f) != neg_prov) {
+    if ((hv < 0.f) != neg_prov && hout) {       // encode mode: flip the packed bit
+      if (lane == 0) atomicXor(hout + row * hout_ldw + (d >> 5), 1u << (d & 31));
+    } else if ((hv < 0.f) != neg_prov) {
       if (lane == 0) dirty[row] = 1u;
       for (int64_t k = lane; k < K; k += 32) {
         const double c = (double)__ldg(Cp + k * Dp + d) * scale;
@@ -1022,7 +1054,8 @@ cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, i
 cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
                               cudaStream_t st) {
   tc_recheck_kernel<<<148 * 4, 256, 0, st>>>(o.X, o.Bt, o.F, o.Fp, o.Cp, o.Dp, o.K, tc_kp(o.K), o.flags,
-                                             o.flag_count, o.flag_cap, shift, o.corr, o.dirty, o.recheck);
+                                             o.flag_count, o.flag_cap, shift, o.corr, o.dirty, o.recheck,
+                                             o.hout, o.hout_ldw);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   tc_finalize_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(N, o.K, tc_kp(o.K), shift, S, o.corr,
@@ -1078,6 +1111,8 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.s_part_cap = o.s_part_slots;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
+  p.hout = o.hout;
+  p.hout_ldw = o.hout_ldw;
   p.flags = o.flags;
   p.flag_count = o.flag_count;
   p.flag_cap = o.flag_cap;

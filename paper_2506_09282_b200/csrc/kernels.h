@@ -83,6 +83,8 @@ struct TcOperands {
   unsigned long long flag_cap;
   long long* corr;                   // [N_p][Kp] fixed-point corrections, zero between calls
   unsigned* dirty;                   // [N_p], zero between calls
+  uint32_t* hout = nullptr;          // encode mode: bit-packed H output (zeroed by the caller)
+  int64_t hout_ldw = 0;
 };
 int tc_tile_n(int mode, int64_t K);   // D-tile width of K4 (80 or 160)
 // Cluster shape of K4 for a mode (HDC_TC_CLUSTER="NxD" overrides, for measurements).
@@ -108,6 +110,12 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
 cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
                               cudaStream_t st);
 int tc_corr_shift(const float* Cp, int64_t n, int64_t D);   // fixed-point shift for |C| (synchronous)
+
+// k_packed.cu: unfused Stage II from bit-packed H (ablation) and class bundling (training)
+cudaError_t launch_packed_similarity(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,
+                                     int64_t K, int32_t* labels, float* scores, cudaStream_t st);
+cudaError_t launch_bundle(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const int32_t* y, int64_t K,
+                          int32_t* counts, float* M, unsigned* err, cudaStream_t st);
 
 // K5: labels[r] = lowest-index argmax of S[r, 0:K).
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);

@@ -41,6 +41,9 @@ def lib():
         L.hdc_model_infer_host.argtypes = [P, P, I64, P, P, P]
         L.hdc_model_partial_scores.argtypes = [P, P, I64, P, P]
         L.hdc_argmax.argtypes = [P, I64, I64, P, P]
+        L.hdc_model_encode.argtypes = [P, P, I64, P, I64, P]
+        L.hdc_similarity_packed.argtypes = [P, I64, I64, I64, P, I64, P, P, P]
+        L.hdc_bundle_classes.argtypes = [P, I64, I64, I64, P, I64, P, P, P]
         L.hdc_model_destroy.argtypes = [P]
         L.hdc_model_dims.argtypes = [P, P, P, P, P]
         L.hdc_model_recheck_count.argtypes = [P]
@@ -57,7 +60,8 @@ def lib():
         L.hdc_version.restype = ctypes.c_char_p
         for name in ("hdc_infer", "hdc_model_create", "hdc_model_infer", "hdc_model_infer_path",
                      "hdc_model_infer_host", "hdc_model_partial_scores", "hdc_argmax",
-                     "hdc_model_destroy", "hdc_model_dims"):
+                     "hdc_model_destroy", "hdc_model_dims", "hdc_model_encode",
+                     "hdc_similarity_packed", "hdc_bundle_classes"):
             getattr(L, name).restype = I32
         _lib = L
     return _lib
@@ -87,13 +91,17 @@ def _ptr(t):
 class Model:
     """A resident model (hdc_model_create): B (F x D) and C (K x D) on the device."""
 
-    def __init__(self, B, C, prec="fp32"):
+    def __init__(self, B, C, prec="fp32", K=None):
+        """C = None makes an encoder-only model (hdc_model_encode; K classes for training)."""
         B = _dev_f32(B, "B")
-        C = _dev_f32(C, "C")
-        if B.dim() != 2 or C.dim() != 2 or B.shape[1] != C.shape[1]:
-            raise ValueError("B must be F x D and C K x D")
+        if C is not None:
+            C = _dev_f32(C, "C")
+            if B.dim() != 2 or C.dim() != 2 or B.shape[1] != C.shape[1]:
+                raise ValueError("B must be F x D and C K x D")
+        elif B.dim() != 2:
+            raise ValueError("B must be F x D")
         self.F, self.D = B.shape
-        self.K = C.shape[0]
+        self.K = C.shape[0] if C is not None else int(K or 1)
         self.prec = prec
         self.device = B.device
         self._h = ctypes.c_void_p()
@@ -115,6 +123,18 @@ class Model:
             _check(lib().hdc_model_infer_path(self._h, _ptr(X), N, _ptr(labels), _ptr(scores),
                                               PATH[path], _stream_ptr(stream, X.device)))
         return labels, scores
+
+    def encode(self, X, H=None, stream=None):
+        """Stage I only: bit-packed H (N x ceil(D/32) int32 words; bit set <=> h = -1)."""
+        X = _dev_f32(X, "X")
+        N = X.shape[0]
+        ldw = (self.D + 31) // 32
+        if H is None:
+            H = torch.empty(N, ldw, dtype=torch.int32, device=X.device)
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_encode(self._h, _ptr(X), N, _ptr(H), H.shape[1],
+                                          _stream_ptr(stream, X.device)))
+        return H
 
     def infer_host(self, X_host, labels_host, scores_host=None, stream=None):
         """End-to-end call on (pinned) host tensors; asynchronous on `stream`."""
@@ -184,3 +204,49 @@ def argmax(S, labels=None, stream=None):
     with torch.cuda.device(S.device):
         _check(lib().hdc_argmax(_ptr(S), N, K, _ptr(labels), _stream_ptr(stream, S.device)))
     return labels
+
+
+def unpack_signs(H, D):
+    """Packed H (N x ldw int32) -> N x D tensor of +-1 (test / inspection helper)."""
+    bits = (H.view(torch.int32).unsqueeze(-1) >> torch.arange(32, device=H.device, dtype=torch.int32)) & 1
+    bits = bits.reshape(H.shape[0], -1)[:, :D]
+    return 1 - 2 * bits.to(torch.int8)
+
+
+def similarity_packed(H, D, C, labels=None, scores=None, return_scores=True, stream=None):
+    """Stage II + argmax over a packed H (the unfused ablation path)."""
+    C = _dev_f32(C, "C")
+    N, ldw = H.shape
+    K = C.shape[0]
+    if labels is None:
+        labels = torch.empty(N, dtype=torch.int32, device=H.device)
+    if scores is None and return_scores:
+        scores = torch.empty(N, K, dtype=torch.float32, device=H.device)
+    with torch.cuda.device(H.device):
+        _check(lib().hdc_similarity_packed(_ptr(H), ldw, N, D, _ptr(C), K, _ptr(labels), _ptr(scores),
+                                           _stream_ptr(stream, H.device)))
+    return labels, scores
+
+
+def bundle_classes(H, D, y, K, counts=None, return_M=True, stream=None):
+    """Single-pass training: counts[k] += sum of h_n over class k; M = HardSign(counts)."""
+    N, ldw = H.shape
+    y = y.to(torch.int32).contiguous()
+    if counts is None:
+        counts = torch.zeros(K, D, dtype=torch.int32, device=H.device)
+    M = torch.empty(K, D, dtype=torch.float32, device=H.device) if return_M else None
+    with torch.cuda.device(H.device):
+        _check(lib().hdc_bundle_classes(_ptr(H), ldw, N, D, _ptr(y), K, _ptr(counts), _ptr(M),
+                                        _stream_ptr(stream, H.device)))
+    return counts, M
+
+
+def train_single_pass(X, y, B, K, prec="fp32_tc"):
+    """Class HVs from labelled data: M = HardSign(sum over class of HardSign(x B))."""
+    m = Model(B, None, prec=prec, K=K)
+    try:
+        H = m.encode(X)
+        counts, M = bundle_classes(H, m.D, y, K)
+    finally:
+        m.close()
+    return M, counts
