@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", default="infer", choices=["infer", "unfused", "train"],
+                    help="infer: fused hot path (default); unfused: the fusion ablation "
+                         "(hdc_model_encode writes bit-packed H to HBM, hdc_similarity_packed "
+                         "reads it back); train: single-pass training (encode + class bundling)")
     ap.add_argument("--dshard", action="store_true",
                     help="D-shard (small-N): each rank holds a column slice; all-reduce of N x K "
                          "partial scores inside the timed step (strong scaling)")
@@ -258,9 +262,19 @@ def run_ours(args, rank, world, local_rank):
     labels = torch.empty(cfg.N, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     Sbuf = torch.empty(cfg.N, cfg.K, dtype=torch.float32, device=dev)
+    Hbuf = torch.empty(cfg.N, (cfg.D + 31) // 32, dtype=torch.int32, device=dev)
+    ytrain = (torch.arange(cfg.N, device=dev, dtype=torch.int32) * 7919) % cfg.K
+    counts = torch.zeros(cfg.K, cfg.D, dtype=torch.int32, device=dev)
 
     def step():
-        if args.dshard:
+        if args.mode == "unfused":
+            model.encode(X, H=Hbuf)
+            hdc.similarity_packed(Hbuf, cfg.D, C, labels=labels, return_scores=False)
+        elif args.mode == "train":
+            model.encode(X, H=Hbuf)
+            counts.zero_()
+            hdc.bundle_classes(Hbuf, cfg.D, ytrain, cfg.K, counts=counts, return_M=False)
+        elif args.dshard:
             model.partial_scores(X, out=Sbuf)
             if world > 1:
                 dist.all_reduce(Sbuf)
@@ -273,7 +287,8 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = model.last_launch_count() + (1 if args.dshard else 0)
+    launches_per_step = model.last_launch_count() + (1 if args.dshard else 0) + \
+        {"infer": 0, "unfused": 2, "train": 4}[args.mode]   # + memset/similarity, memset/sort/bundle
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -314,7 +329,7 @@ def run_ours(args, rank, world, local_rank):
 
     # end to end through the public host-buffer entry point (H2D X, D2H labels)
     e2e = None
-    if not args.no_e2e and not args.dshard:
+    if not args.no_e2e and not args.dshard and args.mode == "infer":
         Xh = X.cpu().pin_memory()
         yh = torch.empty(cfg.N, dtype=torch.int32).pin_memory()
         for _ in range(2):
@@ -356,7 +371,7 @@ def run_ours(args, rank, world, local_rank):
            "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16", "fp32_tc": "i8x3"}[args.prec],
            "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
-                      "prec": args.prec, "path": args.path, "global_batch": units,
+                      "prec": args.prec, "path": args.path, "mode": args.mode, "global_batch": units,
                       "parallelism": ("dshard%d" % world) if args.dshard else ("dp%d" % world),
                       "l2": "flushed between steps (write of 2x L2 bytes, untimed)",
                       "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
