@@ -50,6 +50,12 @@ using namespace ptx;
 
 constexpr int BM = 128;              // rows per tile (MMA M)
 constexpr int STAGES_MAX = 6;
+// K bytes per operand stage for bf16/tf32 (int8 always 64): 64 B (SWIZZLE_64B) halves the
+// stage and doubles the ring depth, so the producer / MMA handshakes of more stages are
+// in flight (measured: each stage hand-off costs ~1 us of barrier latency round trip).
+#ifndef HDC_TC_KB16
+#define HDC_TC_KB16 128
+#endif
 #ifndef HDC_TC_EPI_WARPS
 #define HDC_TC_EPI_WARPS 8
 #endif
@@ -76,8 +82,8 @@ struct Cfg {
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
   // K bytes per stage = one swizzle-atom row: 128 B (SWIZZLE_128B) for the single-operand
   // modes, 64 B (SWIZZLE_64B) for the 3-limb int8 mode (smem budget).
-  static constexpr int KBYTES = (MODE == 2) ? 64 : 128;
-  static constexpr int SWZ = (MODE == 2) ? 4 : 2;                // descriptor layout type
+  static constexpr int KBYTES = (MODE == 2) ? 64 : HDC_TC_KB16;
+  static constexpr int SWZ = (KBYTES == 64) ? 4 : 2;             // descriptor layout type
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
   static constexpr int A_LIMB_BYTES = BM * KBYTES;
   static constexpr int B_LIMB_BYTES = BN * KBYTES;
@@ -148,10 +154,21 @@ struct TcParams {
   unsigned long long* dbg; // [16] cycle counters (debug & 4)
 };
 
+// Diagnostics (HDC_TC_DEBUG ablation / counter flags) exist only in side builds compiled
+// with -DHDC_TC_DIAG=1 (tools/tc_timing.py); the product kernel has no debug branches.
+#ifndef HDC_TC_DIAG
+#define HDC_TC_DIAG 0
+#endif
+#ifndef HDC_I8_EPI_UNROLL
+#define HDC_I8_EPI_UNROLL 1
+#endif
+constexpr int kI8EpiUnroll = HDC_I8_EPI_UNROLL;
+#define DBG(mask) (HDC_TC_DIAG ? (p.debug & (mask)) : 0)
+
 // Timed barrier wait (diagnostics): accumulates the cycles spent waiting.
 #define TWAIT(slot, bar, par)                                        \
   do {                                                               \
-    if (p.debug & 4) {                                               \
+    if (DBG(4)) {                                               \
       const long long _t0 = clock64();                               \
       mbar_wait(bar, par);                                           \
       dbgc[slot] += (unsigned long long)(clock64() - _t0);           \
@@ -199,7 +216,7 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE, int BN, int CLN, int CLD>
+template <int MODE, int BN, int CLN, int CLD, bool ENC>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const TcParams p) {
@@ -272,7 +289,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, NUM_EPI);
       mbar_init(cfull + b, 1);
-      mbar_init(cempty + b, 1);
+      mbar_init(cempty + b, (MODE == 2 && ENC) ? NUM_EPI : 1);   // encode: epilogue frees taus
       mbar_init(hfull + b, NUM_EPI);
       mbar_init(hempty + b, 1);
     }
@@ -300,8 +317,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int64_t t = t0; t < t1; ++t) {
         const int ni = (int)(t / p.TdG) * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
         for (int kb = 0; kb < KB; ++kb) {
-          TWAIT(0, empty + stage, phase ^ 1);
-          if (p.debug & 2) {
+          if (DBG(4096)) mbar_wait_spin(empty + stage, phase ^ 1);
+          else TWAIT(0, empty + stage, phase ^ 1);
+          if ((DBG(1024)) && c == 0) {
+            const int64_t si = (t - t0) * KB + kb;
+            if (si < 256) p.dbg[16 + 256 + si] = (unsigned long long)clock64();
+          }
+          if (DBG(2)) {
             mbar_arrive(full + stage);
           } else {
             mbar_arrive_expect_tx(full + stage, STAGE_TX);   // whole tiles: own + peers' slices
@@ -331,16 +353,21 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint64_t a_desc0 = sdesc(smem_u32(sA));
     const uint64_t b_desc0 = sdesc(smem_u32(sB));
     for (int64_t t = t0; t < t1; ++t) {
-      TWAIT(1, tempty + buf, bphase ^ 1);
+      if (!(DBG(8192))) TWAIT(1, tempty + buf, bphase ^ 1);   // 8192: diagnostics, no epilogue
       tc_fence_after();
       const uint32_t acc0 = tmem_base + buf * CF::ACC_STRIDE;
       for (int kb = 0; kb < KB; ++kb) {
-        TWAIT(2, full + stage, phase);
+        if (DBG(4096)) mbar_wait_spin(full + stage, phase);   // diagnostics: spin
+        else TWAIT(2, full + stage, phase);
+        if ((DBG(1024)) && c == 0 && lane == 0) {
+          const int64_t si = (t - t0) * KB + kb;
+          if (si < 256) p.dbg[16 + si] = (unsigned long long)clock64();
+        }
         tc_fence_after();
         // descriptors = base descriptor + (byte offset >> 4) in the start-address field
         const uint64_t a_d = a_desc0 + (uint64_t)((stage * CF::A_STAGE) >> 4);
         const uint64_t b_d = b_desc0 + (uint64_t)((stage * CF::B_STAGE) >> 4);
-        if (!(p.debug & 1)) {
+        if (!(DBG(1))) {
           const uint32_t acc = (kb == 0) ? 0u : 1u;
           if constexpr (MODE == 2) {
             // The three B limb tiles are contiguous rows [b0; b1; b2] (240 x 64 B) and
@@ -353,12 +380,17 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                 a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
                                 IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
           } else {
-            static_assert(KBYTES / 32 == 4, "4 MMAs per stage");
-            tc_mma4_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
-                                IDESC, acc);
+            if constexpr (KBYTES == 128)
+              tc_mma4_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
+                                  IDESC, acc);
+            else
+              tc_mma2_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, IDESC, acc);
           }
         }
-        if constexpr (CLS > 1) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
+        if ((DBG(2049)) == 2049) {     // diagnostics (no MMAs): plain arrive instead of commit
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + stage);
+        } else if constexpr (CLS > 1) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
         else tc_commit_elect(empty + stage);
         if (++stage == STAGES) {
           stage = 0;
@@ -370,7 +402,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (buf == 0) bphase ^= 1;
     }
   } else if (warp == 2) {
-    if (!p.hout) {   // encode mode: no Stage II, no C tiles
+    if ((!ENC || MODE == 2) && !(DBG(8192))) {   // encode mode: only the int8 column taus
     // ===================================================== C-tile producer (Stage II B operand)
     // A separate warp, so the operand stream never waits for a C slot.
     if (lane == 0) {
@@ -379,8 +411,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int64_t t = t0; t < t1; ++t) {
         const int di = (int)(t % p.TdG) * CLD + rd;
         mbar_wait(cempty + cs, cphase ^ 1);
-        mbar_arrive_expect_tx(cfull + cs, c_tile_bytes + (MODE == 2 ? BN * 8 : 0));   // + taus
-        bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
+        mbar_arrive_expect_tx(cfull + cs, (ENC ? 0u : c_tile_bytes) + (MODE == 2 ? BN * 8 : 0));
+        if (!ENC)
+          bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
         if constexpr (MODE == 2)
           bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
                     cfull + cs);
@@ -390,7 +423,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     }
   } else if (warp == 3) {
-    if (!p.hout) {
+    if (!ENC && !(DBG(8192))) {
     // ===================================================== Stage II MMA issuer (elected lane)
     // A warp of its own: S += H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
     // never waiting behind (or holding up) the Stage I issue loop.
@@ -412,7 +445,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int part = 0; part < 2; ++part) {      // C = hi + lo, both into the same columns
           const uint64_t bd = smem_desc_interleaved(
               c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
-          if (p.debug & 8) continue;
+          if (DBG(8)) continue;
           if constexpr (CF::H_TMEM) {
             // A = H from TMEM (16 bf16 = 8 columns per k-step)
             tc_mma_ts_elect(d2, tmem_base + CF::H_COL + hb * (BN / 2) + s * 8, bd, IDESC2,
@@ -440,7 +473,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (cs == 0) cphase ^= 1;
     }
     }
-  } else if (warp >= EPI_WARP0) {
+  } else if (warp >= EPI_WARP0 && !(DBG(8192))) {
     // ===================================================== epilogue
     const int ew = warp - EPI_WARP0;
     const int q = warp & 3;                 // TMEM lane quarter (hardware: warp id % 4)
@@ -459,18 +492,14 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const bool row_ok = row < p.N;
       int64_t rtau = -1;                    // int8 mode: row part of tau
       if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : -(int64_t(1) << 62);
-      if (p.debug & 256) {                  // diagnostics: sleep-polling instead of try_wait
+      if (DBG(256)) {                  // diagnostics: sleep-polling instead of try_wait
         while (!mbar_test(tfull + buf, bphase)) __nanosleep(500);
       }
       TWAIT(6, tfull + buf, bphase);
       const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
       if constexpr (MODE == 2) {
-        if (p.hout) {
-          sct = p.coltau + (int64_t)di * BN;   // encode mode: no C tiles; taus from global
-        } else {
-          TWAIT(15, cfull + cs, cphase);
-          sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
-        }
+        TWAIT(15, cfull + cs, cphase);
+        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
       }
       tc_fence_after();
       // ---- phase 1: accumulator -> HardSign bits (bit set -> h = -1) and recheck flags
@@ -478,10 +507,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
       for (int w = 0; w < NWB; ++w) hbits[w] = flags[w] = 0u;
       const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE + cq * EPI_COLS;
-#pragma unroll
-      for (int ch = 0; ch < ((p.debug & 16) ? 0 : EPI_COLS / CH); ++ch) {
-        const int cl = ch * CH;             // column within this thread's group
-        if constexpr (MODE == 2) {
+      if constexpr (MODE == 2) {
+        // 64-bit masks (EPI_COLS <= 64): register-resident under any unrolling
+        static_assert(EPI_COLS <= 64, "int8 column group");
+        uint64_t hb64 = 0, fl64 = 0;
+#pragma unroll kI8EpiUnroll
+        for (int ch = 0; ch < ((DBG(16)) ? 0 : EPI_COLS / CH); ++ch) {
+          const int cl = ch * CH;             // column within this thread's group
           uint32_t r0[CH], r1[CH], r2[CH];
           if constexpr (CH == 16) {
             tmem_ld16(tbase + cl, r0);
@@ -498,11 +530,21 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
                               (int64_t)(int32_t)r2[j];
             const int b = cl + j;
-            if (I < 0) hbits[b >> 5] |= 1u << (b & 31);
             const int64_t aI = I < 0 ? -I : I;
-            if (aI <= rtau + sct[cq * EPI_COLS + b]) flags[b >> 5] |= 1u << (b & 31);   // tau = -inf past D
+            hb64 |= (uint64_t)(I < 0) << b;
+            fl64 |= (uint64_t)(aI <= rtau + sct[cq * EPI_COLS + b]) << b;   // tau = -inf past D
           }
-        } else {
+        }
+        hbits[0] = (uint32_t)hb64;
+        flags[0] = (uint32_t)fl64;
+        if constexpr (NWB > 1) {
+          hbits[1] = (uint32_t)(hb64 >> 32);
+          flags[1] = (uint32_t)(fl64 >> 32);
+        }
+      } else {
+#pragma unroll
+        for (int ch = 0; ch < ((DBG(16)) ? 0 : EPI_COLS / CH); ++ch) {
+          const int cl = ch * CH;             // column within this thread's group
           uint32_t r0[CH];
           if constexpr (CH == 16) tmem_ld16(tbase + cl, r0);
           else tmem_ld8(tbase + cl, r0);
@@ -516,9 +558,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + buf);   // accumulator free for tile t + 2
+      if (lane == 0) {
+        mbar_arrive(tempty + buf);                // accumulator free for tile t + 2
+        if (MODE == 2 && ENC) mbar_arrive(cempty + cs);   // encode mode: taus read
+      }
       // H buffer hb free (Stage II of tile t - 2 done)
-      if (!p.hout) {
+      if constexpr (!ENC) {
         TWAIT(7, hempty + hb, hphase ^ 1);
         tc_fence_after();
       }
@@ -529,7 +574,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if constexpr (MODE == 2) {
 #pragma unroll
         for (int w = 0; w < NWB; ++w) {
-          uint32_t fw = (p.debug & 512) ? 0u : flags[w];   // 512: diagnostics, no rechecks
+          uint32_t fw = (DBG(512)) ? 0u : flags[w];   // 512: diagnostics, no rechecks
           uint32_t spill = 0u;
           while (fw) {
             const int bit = __ffs(fw) - 1;
@@ -559,7 +604,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
       // ---- phase 3: H (exact bf16 +-1: 0x3F80 / 0xBF80) for the Stage II MMA
-      if (p.hout) {
+      if constexpr (ENC) {
         // encode mode: OR this thread's sign bits into the packed rows (column groups of
         // neighbouring threads / tiles share words; OR of disjoint bits is order-free)
         if (row_ok) {
@@ -576,7 +621,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (sh && wi + 1 < p.hout_ldw && (bits >> (32 - sh))) atomicOr(hr + wi + 1, bits >> (32 - sh));
           }
         }
-      } else if (p.debug & 128) {
+      } else if (DBG(128)) {
         // diagnostics: no H write
       } else if constexpr (CF::H_TMEM) {
         // packed bf16 pairs into TMEM columns H_COL + col / 2 of this thread's lane
@@ -626,7 +671,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && !p.hout) mbar_arrive(hfull + hb);
+      if (lane == 0 && !ENC) mbar_arrive(hfull + hb);
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
       if (++hb == NH) {
@@ -636,7 +681,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       cs ^= 1;
       if (cs == 0) cphase ^= 1;
 
-      if (p.hout || !seg_last(t, t1, p.TdG)) continue;
+      if (ENC || !seg_last(t, t1, p.TdG)) continue;
       // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM.  The
       // N-tile's D-groups are split over clusters c_first..c_last, each over its CLD ranks.
       const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G);
@@ -715,7 +760,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
-  if ((p.debug & 4) && lane == 0 && (warp <= 3 || warp == EPI_WARP0)) {
+  if ((DBG(4)) && lane == 0 && (warp <= 3 || warp == EPI_WARP0)) {
     if (warp != EPI_WARP0) dbgc[15] = 0;
     dbgc[warp == EPI_WARP0 ? 12 : (warp == 3 ? 13 : 9 + warp)] = (unsigned long long)(clock64() - t_start);
     for (int i = 0; i < 16; ++i)
@@ -928,12 +973,12 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int BN, int CLN, int CLD>
+template <int MODE, int BN, int CLN, int CLD, bool ENC>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p, int num_sms,
                         cudaStream_t st) {
   constexpr int CLS = CLN * CLD;
   const size_t sm = Cfg<MODE, BN>::TOTAL + 1024;
-  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD>;
+  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -968,15 +1013,21 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
   return cudaGetLastError();
 }
 
+template <int MODE, int BN, bool ENC>
+cudaError_t launch_cluster_e(int cl_n, int cl_d, const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
+                             int num_sms, cudaStream_t st) {
+  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC>(a, b, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC>(a, b, p, num_sms, st);
+  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC>(a, b, p, num_sms, st);
+  return cudaErrorInvalidValue;
+}
+// ENC (encode mode, hdc_model_encode) is a separate instantiation so the inference kernel
+// carries no encode branches.
 template <int MODE, int BN>
 cudaError_t launch_cluster(int cl_n, int cl_d, const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
                            int num_sms, cudaStream_t st) {
-  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1>(a, b, p, num_sms, st);
-  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2>(a, b, p, num_sms, st);
-  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1>(a, b, p, num_sms, st);
-  if (cl_n == 2 && cl_d == 2) return launch_mode<MODE, BN, 2, 2>(a, b, p, num_sms, st);
-  if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4>(a, b, p, num_sms, st);
-  return cudaErrorInvalidValue;
+  return p.hout ? launch_cluster_e<MODE, BN, true>(cl_n, cl_d, a, b, p, num_sms, st)
+                : launch_cluster_e<MODE, BN, false>(cl_n, cl_d, a, b, p, num_sms, st);
 }
 
 }  // namespace
@@ -997,7 +1048,7 @@ void tc_cluster_shape(int mode, int64_t K, int* cl_n, int* cl_d) {
   const char* env = getenv("HDC_TC_CLUSTER");
   int en = 0, ed = 0;
   if (env && sscanf(env, "%dx%d", &en, &ed) == 2 &&
-      ((en == 1 && (ed == 1 || ed == 2 || ed == 4)) || (en == 2 && (ed == 1 || ed == 2))) &&
+      ((en == 1 && (ed == 1 || ed == 2)) || (en == 2 && ed == 1)) &&
       !(tile_n_for(mode, K) == 80 && mode != 2)) {
     n = en;
     d = ed;
@@ -1124,9 +1175,9 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   }
   static unsigned long long* dbg_buf = nullptr;
   p.dbg = nullptr;
-  if (p.debug & 4) {
-    if (!dbg_buf) cudaMalloc((void**)&dbg_buf, 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(dbg_buf, 0, 16 * sizeof(unsigned long long), st);
+  if (p.debug & (4 | 1024)) {
+    if (!dbg_buf) cudaMalloc((void**)&dbg_buf, (16 + 512) * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_buf, 0, (16 + 512) * sizeof(unsigned long long), st);
     p.dbg = dbg_buf;
   }
   const int nl = (mode == 2) ? 3 : 1;
@@ -1135,8 +1186,8 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUtensorMap ma, mb;
-  const uint32_t kbytes = (mode == 2) ? 64 : 128;
-  const CUtensorMapSwizzle swz = (mode == 2) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const uint32_t kbytes = (mode == 2) ? 64 : HDC_TC_KB16;
+  const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
   if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, BM / o.cl_d, swz) ||
       !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, bn / o.cl_n, swz))
@@ -1146,8 +1197,19 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
   else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
   else if (o.cl_n == 1 && o.cl_d == 1)
-    e = (mode == 0) ? launch_mode<0, 80, 1, 1>(ma, mb, p, num_sms, st) : launch_mode<1, 80, 1, 1>(ma, mb, p, num_sms, st);
+    e = (mode == 0) ? (p.hout ? launch_mode<0, 80, 1, 1, true>(ma, mb, p, num_sms, st)
+                              : launch_mode<0, 80, 1, 1, false>(ma, mb, p, num_sms, st))
+                    : (p.hout ? launch_mode<1, 80, 1, 1, true>(ma, mb, p, num_sms, st)
+                              : launch_mode<1, 80, 1, 1, false>(ma, mb, p, num_sms, st));
   else e = cudaErrorInvalidValue;
+  if (e == cudaSuccess && (p.debug & 1024)) {
+    unsigned long long h[512];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg_buf + 16, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[hdc tc timeline] CTA 0, KB=%d stages/tile; MMA full-wait exits / producer empty-wait exits (cycles from first):\n", (int)(p.Fp / (mode == 2 ? 64 : (mode == 0 ? 64 : 32))));
+    for (int i = 0; i < 64; ++i)
+      fprintf(stderr, "  stage %3d: mma %8lld  prod %8lld\n", i, (long long)(h[i] - h[0]), (long long)(h[256 + i] - h[0]));
+  }
   if (e == cudaSuccess && (p.debug & 4)) {
     unsigned long long h[16];
     cudaStreamSynchronize(st);

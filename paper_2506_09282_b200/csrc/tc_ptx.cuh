@@ -66,6 +66,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Spin (never suspends): for the latency-critical operand ring waits.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 // Non-blocking probe: true iff the phase with parity `parity` has completed.
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -246,6 +258,22 @@ __device__ __forceinline__ void tc_mma4_elect(uint32_t d, uint64_t a0, uint64_t 
   else if constexpr (KIND == 1) HDC_MMA4("kind::tf32");
   else HDC_MMA4("kind::i8");
 #undef HDC_MMA4
+}
+
+template <int KIND>
+__device__ __forceinline__ void tc_mma2_elect(uint32_t d, uint64_t a0, uint64_t b0, uint64_t a1, uint64_t b1,
+                                              uint32_t idesc, uint32_t accumulate) {
+#define HDC_MMA2(KS)                                                                          \
+  asm volatile(                                                                             \
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\t"    \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %1, %2, %5, p;\n\t"                           \
+      "@e tcgen05.mma.cta_group::1." KS " [%0], %3, %4, %5, 1;\n\t}" ::"r"(d),                \
+      "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate)                          \
+      : "memory")
+  if constexpr (KIND == 0) HDC_MMA2("kind::f16");
+  else if constexpr (KIND == 1) HDC_MMA2("kind::tf32");
+  else HDC_MMA2("kind::i8");
+#undef HDC_MMA2
 }
 
 // One int8 k-step of the 3-limb scheme (see k_fused_tc.cu): three MMAs, one elect.

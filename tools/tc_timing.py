@@ -1,4 +1,6 @@
-"""Diagnostics: dominant-kernel time of K4 under HDC_TC_DEBUG ablation flags
+"""Diagnostics: dominant-kernel time of K4 under HDC_TC_DEBUG ablation flags.
+The flags act only in the diagnostics build (HDC_BUILD_TAG=diag HDC_NVCC_DEFS=-DHDC_TC_DIAG=1
+python -m paper_2506_09282_b200.build; run with HDC_LIB_PATH=.../lib/libhdc_diag.so)
 (1 = no Stage I MMA, 2 = no operand TMA, 8 = no Stage II MMA, 16 = no epilogue
 TMEM reads, 32 = Stage II only at tile boundaries).  Results of ablated runs are
 wrong by construction; only their timing is of interest."""
