@@ -6,9 +6,9 @@
 #include "../paper_2506_09282_b200/csrc/tc_ptx.cuh"
 using namespace hdc::ptx;
 
-template <int N, int VARIANT, bool RANDOM = false>   // VARIANT 0: elect-issue (kernel), 1: lane-0 issue, 2: elect, fixed D,
+template <int N, int VARIANT, bool RANDOM = false, int NT = 128>   // VARIANT 0: elect-issue (kernel), 1: lane-0 issue, 2: elect, fixed D,
                                                      // 3: no MMA (commit only), 4: no MMA, plain arrive
-__global__ void ring2(int iters, unsigned long long* out) {
+__global__ void __launch_bounds__(NT, 1) ring2(int iters, unsigned long long* out) {
   constexpr int STAGES = 5, A_ST = 16384, B_ST = N * 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -77,16 +77,16 @@ __global__ void ring2(int iters, unsigned long long* out) {
   if (warp == 1) tmem_dealloc<512>(tb);
 }
 
-template <int N, int VARIANT, bool RANDOM = false>
+template <int N, int VARIANT, bool RANDOM = false, int NT = 128>
 void run(const char* name, int iters = 4000) {
   const int blocks = 148;
   unsigned long long* d;
   cudaMalloc(&d, sizeof(unsigned long long) * blocks * 2);
-  auto k = ring2<N, VARIANT, RANDOM>;
+  auto k = ring2<N, VARIANT, RANDOM, NT>;
   const int sm = 5 * (16384 + N * 128) + 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  k<<<blocks, 128, sm>>>(iters, d);
-  k<<<blocks, 128, sm>>>(iters, d);
+  k<<<blocks, NT, sm>>>(iters, d);
+  k<<<blocks, NT, sm>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[296];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -103,6 +103,8 @@ int main() {
   run<160, 2>("N=160 elect, D fixed");
   run<80, 0>("N=80 elect, D alternating");
   run<160, 3>("no MMA, commit per stage");
+  run<160, 3, false, 384>("no MMA, commit per stage, 384 threads");
+  run<160, 0, false, 384>("N=160 elect, 384 threads");
   run<160, 4>("no MMA, plain arrive per stage");
   run<160, 0, true>("N=160 elect, random data");
   run<160, 0, false>("N=160 elect, zero data, long", 200000);
