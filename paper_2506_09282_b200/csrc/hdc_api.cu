@@ -55,6 +55,7 @@ struct hdc_model_s {
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
   int64_t Dq = 0;            // D rounded up to cl_d tensor-core D tiles (tc_tile_n)
   int cl_n = 1, cl_d = 1;    // K4 thread-block cluster (multicast) shape
+  int cl_virt = 0;           // 1: virtual 1 x cl_d CTA groups (large F: L2 working set)
   void* Btc = nullptr;       // [NL][Dq][Fp]
   int64_t* coltau = nullptr; // [Dq] (int8 limbs)
   void* Cil = nullptr;       // per D-tile Stage II operand (tc_c_tile_bytes each)
@@ -227,7 +228,7 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   const int64_t gm = kTileM * m->cl_n;
   const int64_t Np = (N + gm - 1) / gm * gm;
   const int64_t slots = tc_s_part_slots(Np / kTileM, m->Dq / tc_tile_n(mode, m->K), m->cl_n, m->cl_d,
-                                        m->num_sms);
+                                        m->cl_virt, m->num_sms);
   if (Np <= m->tw_rows && slots <= m->tw_slots) return HDC_OK;
   const int64_t rows = Np > m->tw_rows ? Np : m->tw_rows;
   const int64_t nsl = slots > m->tw_slots ? slots : m->tw_slots;
@@ -299,6 +300,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.N_p = Np;
   o.cl_n = m->cl_n;
   o.cl_d = m->cl_d;
+  o.cl_virt = m->cl_virt;
   o.A = m->Atc;
   o.B = m->Btc;
   o.Cil = m->Cil;
@@ -468,7 +470,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 64);
   const int mode = tc_mode_of(m);
   const int64_t tn = tc_tile_n(mode < 0 ? 0 : mode, K);
-  tc_cluster_shape(mode < 0 ? 0 : mode, K, &m->cl_n, &m->cl_d);
+  tc_cluster_shape(mode < 0 ? 0 : mode, K, F, D, &m->cl_n, &m->cl_d, &m->cl_virt);
   m->Dq = (D + tn * m->cl_d - 1) / (tn * m->cl_d) * (tn * m->cl_d);
   if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
     e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);

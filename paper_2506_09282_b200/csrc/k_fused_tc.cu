@@ -216,7 +216,7 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC>
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const TcParams p) {
@@ -262,10 +262,15 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // dg CLD + rd of cluster tile (ng, dg).  The CLD CTAs sharing an N-tile multicast
   // its X tile (each loads 128/CLD rows), the CLN CTAs sharing a D-tile multicast its
   // B tile (BN/CLN rows each): L2 -> SM traffic per tile falls by those factors.
+  // HWC = false: a "virtual" cluster -- CLS consecutive CTAs share the tile schedule (the
+  // CLD ranks work on the same N-tile at the same time, so its X tile is read from L2 by
+  // all of them while few N-tiles are live: the L2 working set when X tiles are large,
+  // DESIGN.md §2) but load their own tiles, with no hardware cluster or multicast.
   constexpr int CLS = CLN * CLD;
+  constexpr bool MC = HWC && CLS > 1;              // hardware cluster with multicast
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;                        // global CTA index (partial-score slots)
-  const int rank = (CLS > 1) ? (int)cluster_ctarank() : 0;
+  const int rank = MC ? (int)cluster_ctarank() : (CLS > 1 ? c % CLS : 0);
   const int rn = rank / CLD, rd = rank % CLD;
   const int cl = c / CLS;                          // cluster index
   const uint16_t a_mask = (uint16_t)(((1u << CLD) - 1u) << (rn * CLD));   // same N-tile
@@ -283,7 +288,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, CLN + CLD - 1);   // MMA commits of every CTA this one multicasts to
+      mbar_init(empty + s, MC ? CLN + CLD - 1 : 1);   // MMA commits of every CTA this one multicasts to
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
@@ -303,7 +308,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  if constexpr (CLS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  if constexpr (MC) cluster_sync_all();   // peers' barriers initialised before any multicast
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -313,7 +318,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      constexpr int AR = BM / CLD, BR = BN / CLN;    // rows of the A / B tile this CTA loads
+      constexpr int AR = MC ? BM / CLD : BM, BR = MC ? BN / CLN : BN;   // rows this CTA loads
+      const int ra = MC ? rd : 0, rb = MC ? rn : 0;       // its slice of the A / B tile
       for (int64_t t = t0; t < t1; ++t) {
         const int ni = (int)(t / p.TdG) * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
         for (int kb = 0; kb < KB; ++kb) {
@@ -329,13 +335,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_arrive_expect_tx(full + stage, STAGE_TX);   // whole tiles: own + peers' slices
 #pragma unroll
             for (int l = 0; l < NL; ++l) {
-              uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + rd * AR * KBYTES;
-              const int ya = (int)(l * p.Np + (int64_t)ni * BM + rd * AR);
-              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + rn * BR * KBYTES;
-              const int yb = (int)(l * p.Dq + (int64_t)di * BN + rn * BR);
-              if constexpr (CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, kb * KE, ya, a_mask);
+              uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + ra * AR * KBYTES;
+              const int ya = (int)(l * p.Np + (int64_t)ni * BM + ra * AR);
+              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + rb * BR * KBYTES;
+              const int yb = (int)(l * p.Dq + (int64_t)di * BN + rb * BR);
+              if constexpr (MC && CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, kb * KE, ya, a_mask);
               else tma_load_2d(da, &tmA, full + stage, kb * KE, ya);
-              if constexpr (CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, kb * KE, yb, b_mask);
+              if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, kb * KE, yb, b_mask);
               else tma_load_2d(db, &tmB, full + stage, kb * KE, yb);
             }
           }
@@ -390,7 +396,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if ((DBG(2049)) == 2049) {     // diagnostics (no MMAs): plain arrive instead of commit
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + stage);
-        } else if constexpr (CLS > 1) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
+        } else if constexpr (MC) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
         else tc_commit_elect(empty + stage);
         if (++stage == STAGES) {
           stage = 0;
@@ -767,7 +773,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (dbgc[i]) atomicAdd(p.dbg + i, dbgc[i]);
   }
   __syncwarp();
-  if constexpr (CLS > 1) cluster_sync_all();   // no CTA leaves while peers may still signal it
+  if constexpr (MC) cluster_sync_all();   // no CTA leaves while peers may still signal it
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -973,12 +979,12 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC>
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC = true>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p, int num_sms,
                         cudaStream_t st) {
   constexpr int CLS = CLN * CLD;
   const size_t sm = Cfg<MODE, BN>::TOTAL + 1024;
-  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC>;
+  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC, HWC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -987,7 +993,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CLS;
+  attr[0].val.clusterDim.x = HWC ? CLS : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -997,7 +1003,9 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
   if (max_clusters < 0) {
     cfg.gridDim = dim3(CLS * (num_sms / CLS), 1, 1);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    if (!HWC) {
+      n = num_sms / CLS;                          // one CTA per SM, CLS CTAs per virtual cluster
+    } else if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
       cudaGetLastError();
       n = num_sms / CLS;
     }
@@ -1014,8 +1022,13 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
 }
 
 template <int MODE, int BN, bool ENC>
-cudaError_t launch_cluster_e(int cl_n, int cl_d, const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
-                             int num_sms, cudaStream_t st) {
+cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
+                             TcParams& p, int num_sms, cudaStream_t st) {
+  if (virt) {
+    if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false>(a, b, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false>(a, b, p, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
   if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC>(a, b, p, num_sms, st);
   if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC>(a, b, p, num_sms, st);
   if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC>(a, b, p, num_sms, st);
@@ -1024,37 +1037,56 @@ cudaError_t launch_cluster_e(int cl_n, int cl_d, const CUtensorMap& a, const CUt
 // ENC (encode mode, hdc_model_encode) is a separate instantiation so the inference kernel
 // carries no encode branches.
 template <int MODE, int BN>
-cudaError_t launch_cluster(int cl_n, int cl_d, const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
-                           int num_sms, cudaStream_t st) {
-  return p.hout ? launch_cluster_e<MODE, BN, true>(cl_n, cl_d, a, b, p, num_sms, st)
-                : launch_cluster_e<MODE, BN, false>(cl_n, cl_d, a, b, p, num_sms, st);
+cudaError_t launch_cluster(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
+                           TcParams& p, int num_sms, cudaStream_t st) {
+  return p.hout ? launch_cluster_e<MODE, BN, true>(cl_n, cl_d, virt, a, b, p, num_sms, st)
+                : launch_cluster_e<MODE, BN, false>(cl_n, cl_d, virt, a, b, p, num_sms, st);
 }
 
 }  // namespace
 
 int tc_tile_n(int mode, int64_t K) { return tile_n_for(mode, K); }
-int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int num_sms) {
+int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int virt, int num_sms) {
   if (cl_d == 1) return 2 * (int64_t)num_sms;
   const int64_t T = (Tn / cl_n) * (Td / cl_d), TdG = Td / cl_d;
-  const int64_t gmin = num_sms / (cl_n * cl_d) / 2 > 0 ? num_sms / (cl_n * cl_d) / 2 : 1;  // >= half co-resident
+  int64_t gmin = num_sms / (cl_n * cl_d) / 2 > 0 ? num_sms / (cl_n * cl_d) / 2 : 1;  // >= half co-resident
+  if (virt) gmin = num_sms / (cl_n * cl_d);       // virtual clusters: exactly this many
   const int64_t per = (T + gmin - 1) / gmin;
   return (int64_t)num_sms * ((per + TdG - 1) / TdG + 1);
 }
-void tc_cluster_shape(int mode, int64_t K, int* cl_n, int* cl_d) {
+void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int* cl_d, int* virt) {
   // default: CTA pairs on two N-tiles of the same D-tile, multicasting the B tile
-  // (measured best of 1x1 / 1x2 / 2x1 / 2x2 / 1x4 at cfg2, tools/tc_timing.py)
-  int n = 2, d = 1;
-  if (tile_n_for(mode, K) == 80 && mode != 2) n = 1;   // (bf16/tf32 with K > 32: no cluster)
+  // (measured best of 1x1 / 1x2 / 2x1 / 2x2 / 1x4 hardware clusters at cfg2, tools/tc_timing.py).
+  // When the live X tiles of 148 CTAs plus B exceed the L2 (large F: cfg5 read 176 GB from
+  // DRAM per launch), a virtual 1 x g group puts g CTAs on each N-tile (g = 4, 8).
+  const int bn = tile_n_for(mode, K);
+  int n = 2, d = 1, v = 0;
+  if (bn == 80 && mode != 2) n = 1;               // (bf16/tf32 with K > 32: no cluster)
+  const int64_t Fp = (F + 63) / 64 * 64;
+  const double esz_nl = (mode == 2) ? 3.0 : (mode == 0 ? 2.0 : 4.0);
+  const double a_tile = 128.0 * Fp * esz_nl, b_all = (double)(D + bn) * Fp * esz_nl;
+  const double l2 = 120e6;                        // of the 126 MB L2, leaving room for C, S
+  if (148.0 * a_tile + b_all > l2) {
+    n = 1;
+    v = 1;
+    d = (37.0 * a_tile + b_all <= l2) ? 4 : 8;
+  }
   const char* env = getenv("HDC_TC_CLUSTER");
   int en = 0, ed = 0;
-  if (env && sscanf(env, "%dx%d", &en, &ed) == 2 &&
-      ((en == 1 && (ed == 1 || ed == 2)) || (en == 2 && ed == 1)) &&
-      !(tile_n_for(mode, K) == 80 && mode != 2)) {
-    n = en;
-    d = ed;
+  char vc = 0;
+  if (env) {
+    const int got = sscanf(env, "%dx%d%c", &en, &ed, &vc);
+    if (got >= 2 && !(bn == 80 && mode != 2)) {
+      if (got == 3 && vc == 'v' && en == 1 && (ed == 4 || ed == 8)) {
+        n = 1; d = ed; v = 1;
+      } else if (got == 2 && ((en == 1 && (ed == 1 || ed == 2)) || (en == 2 && ed == 1))) {
+        n = en; d = ed; v = 0;
+      }
+    }
   }
   *cl_n = n;
   *cl_d = d;
+  *virt = v;
 }
 int tc_max_k(int mode) { return mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
 int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
@@ -1189,13 +1221,14 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   const uint32_t kbytes = (mode == 2) ? 64 : HDC_TC_KB16;
   const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
-  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, BM / o.cl_d, swz) ||
-      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, bn / o.cl_n, swz))
+  const int a_rows = o.cl_virt ? BM : BM / o.cl_d, b_rows = o.cl_virt ? bn : bn / o.cl_n;
+  if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, a_rows, swz) ||
+      !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, b_rows, swz))
     return cudaErrorInvalidValue;
   cudaError_t e;
-  if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
-  else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
-  else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, ma, mb, p, num_sms, st);
+  if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
+  else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
+  else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
   else if (o.cl_n == 1 && o.cl_d == 1)
     e = (mode == 0) ? (p.hout ? launch_mode<0, 80, 1, 1, true>(ma, mb, p, num_sms, st)
                               : launch_mode<0, 80, 1, 1, false>(ma, mb, p, num_sms, st))

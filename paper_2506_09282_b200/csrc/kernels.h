@@ -65,6 +65,7 @@ cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, cons
 struct TcOperands {
   int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to cl_d D-tiles; N_p to cl_n x 128 rows
   int cl_n, cl_d;                    // thread-block cluster shape (N-tiles x D-tiles), multicast
+  int cl_virt;                       // 1: virtual 1 x cl_d group (no hardware cluster / multicast)
   const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
   const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
   const void* Cil;                   // per D-tile Stage II operand (tc_c_tile_bytes each)
@@ -88,9 +89,9 @@ struct TcOperands {
 };
 int tc_tile_n(int mode, int64_t K);   // D-tile width of K4 (80 or 160)
 // Cluster shape of K4 for a mode (HDC_TC_CLUSTER="NxD" overrides, for measurements).
-void tc_cluster_shape(int mode, int64_t K, int* cl_n, int* cl_d);
+void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int* cl_d, int* virt);
 // Partial-score slots ([128][K] each) K4 needs for Tn x Td tiles with that cluster shape.
-int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int num_sms);
+int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int virt, int num_sms);
 int tc_max_k(int mode);
 int64_t tc_kp(int64_t K);
 int64_t tc_c_tile_bytes(int mode, int64_t K);
