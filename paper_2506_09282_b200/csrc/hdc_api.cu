@@ -55,7 +55,7 @@ struct hdc_model_s {
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
   int64_t Dq = 0;            // D rounded up to cl_d tensor-core D tiles (tc_tile_n)
   int cl_n = 1, cl_d = 1;    // K4 thread-block cluster (multicast) shape
-  int cl_virt = 0;           // 1: virtual 1 x cl_d CTA groups (large F: L2 working set)
+  int cl_virt = 0;           // 1: virtual 1 x cl_d CTA groups (large F: L2 working set); 2: CTA pair
   void* Btc = nullptr;       // [NL][Dq][Fp]
   int64_t* coltau = nullptr; // [Dq] (int8 limbs)
   void* Cil = nullptr;       // per D-tile Stage II operand (tc_c_tile_bytes each)
@@ -580,7 +580,8 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
   // (Alg. 1 per sample), so chunking changes nothing in the results.
   int nchunks = 1;
   if (N > kSmallMaxN) {
-    const int64_t target = 4096;                      // rows per chunk (>= one full wave of tiles)
+    const char* ev = getenv("HDC_HOST_CHUNK_ROWS");   // diagnostics override
+    const int64_t target = ev ? atoll(ev) : 4096;     // rows per chunk (>= one full wave of tiles)
     nchunks = (int)((N + target - 1) / target);
     if (nchunks > kHostChunksMax) nchunks = kHostChunksMax;
   }

@@ -165,10 +165,39 @@ struct TcParams {
 constexpr int kI8EpiUnroll = HDC_I8_EPI_UNROLL;
 #define DBG(mask) (HDC_TC_DIAG ? (p.debug & (mask)) : 0)
 
+// Watchdog wait (diagnostics, debug & 16384): a wait that has not completed after ~1 s
+// records (slot, CTA, warp, parity) in the host-mapped p.dbg buffer and sets an abort
+// flag on which every later watchdog wait returns at once, so a protocol deadlock ends
+// the kernel (with garbage results) and names the barrier instead of hanging the GPU.
+template <class P>
+__device__ __noinline__ void watchdog_wait(const P& p, uint64_t* bar, uint32_t par, int slot, long long t0) {
+  volatile unsigned long long* d = p.dbg;
+  const long long w0 = clock64();
+  while (!mbar_test(bar, par)) {
+    if (d[0]) return;
+    if (clock64() - w0 > 2000000000ll) {
+      const unsigned long long i =
+          (threadIdx.x & 31) ? ~0ull : atomicAdd((unsigned long long*)p.dbg + 1, 1ull);
+      if (i < 64) {
+        unsigned long long* r = (unsigned long long*)p.dbg + 8 + 4 * i;
+        r[0] = (unsigned long long)slot;
+        r[1] = blockIdx.x;
+        r[2] = threadIdx.x >> 5;
+        r[3] = ((unsigned long long)par << 32) | (unsigned long long)((w0 - t0) >> 10);
+      }
+      __threadfence_system();
+      d[0] = 1;
+      return;
+    }
+  }
+}
+
 // Timed barrier wait (diagnostics): accumulates the cycles spent waiting.
 #define TWAIT(slot, bar, par)                                        \
   do {                                                               \
-    if (DBG(4)) {                                               \
+    if (DBG(16384)) {                                                \
+      watchdog_wait(p, bar, par, slot, t_start);                     \
+    } else if (DBG(4)) {                                             \
       const long long _t0 = clock64();                               \
       mbar_wait(bar, par);                                           \
       dbgc[slot] += (unsigned long long)(clock64() - _t0);           \
@@ -216,11 +245,17 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC>
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const TcParams p) {
+                const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   using CF = Cfg<MODE, BN>;
+  // PAIR: the 2 CTAs of a cluster run as one cta_group::2 MMA unit (M = 256: N-tiles
+  // 2ng, 2ng+1; each CTA holds its 128 X rows and HALF of the B tile and of the C tile in
+  // its own shared memory, so each SM ingests 128 + BN/2 operand rows per k-step instead of
+  // 128 + BN).  The leader (rank 0) issues every MMA; the peer's epilogue signals the
+  // leader's barriers remotely.
+  static_assert(!PAIR || (CLN == 2 && CLD == 1 && HWC && MODE != 2 && !ENC), "pair mode: bf16/tf32 inference, 2x1 cluster");
   constexpr int NL = CF::NL;
   constexpr int KE = CF::KE;
   constexpr int NH = CF::NH;
@@ -279,6 +314,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   for (int i = 0; i < CLN; ++i) b_mask |= (uint16_t)(1u << (i * CLD + rd));
   const int64_t t0 = range_begin(cl, p.T, p.G), t1 = range_begin(cl + 1, p.T, p.G);
   const int KB = (int)(p.Fp / KE);
+  const bool leader = !PAIR || rank == 0;
+  // pair mode: barriers the leader's MMA warps wait on are the leader's
+  auto arrive_lead = [&](uint64_t* bar) {
+    if constexpr (PAIR) mbar_arrive_cluster(mapa_u32(bar, 0));
+    else mbar_arrive(bar);
+  };
   unsigned long long dbgc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) dbgc[i] = 0;
@@ -288,25 +329,28 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, MC ? CLN + CLD - 1 : 1);   // MMA commits of every CTA this one multicasts to
+      mbar_init(empty + s, (MC && !PAIR) ? CLN + CLD - 1 : 1);   // MMA commits of every CTA this one multicasts to
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, NUM_EPI);
+      mbar_init(tempty + b, PAIR ? 2 * NUM_EPI : NUM_EPI);   // pair: both CTAs' epilogues
       mbar_init(cfull + b, 1);
       mbar_init(cempty + b, (MODE == 2 && ENC) ? NUM_EPI : 1);   // encode: epilogue frees taus
-      mbar_init(hfull + b, NUM_EPI);
+      mbar_init(hfull + b, PAIR ? 2 * NUM_EPI : NUM_EPI);
       mbar_init(hempty + b, 1);
     }
     mbar_init(sfull, 1);
-    mbar_init(sempty, 4);               // the 4 warps of column group 0 drain S
+    mbar_init(sempty, PAIR ? 8 : 4);    // the 4 warps of column group 0 (of each CTA) drain S
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   if constexpr (MC) cluster_sync_all();   // peers' barriers initialised before any multicast
   else __syncthreads();
@@ -332,6 +376,15 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (DBG(2)) {
             mbar_arrive(full + stage);
           } else {
+            if constexpr (PAIR) {
+              // both CTAs' loads complete on the leader's barrier (the leader's MMA waits on it)
+              const uint32_t fbar = mapa_u32(full + stage, 0);
+              // (the leader's own barrier: a CTA-scope arrive, no cluster-scope release fence)
+              if (leader) mbar_arrive_expect_tx(full + stage, 2 * (CF::A_LIMB_BYTES + (BN / 2) * KBYTES));
+              tma_load_2d_pair(sA + stage * CF::A_STAGE, &tmA, fbar, kb * KE, (int)((int64_t)ni * BM));
+              tma_load_2d_pair(sB + stage * CF::B_STAGE, &tmB, fbar, kb * KE,
+                               (int)((int64_t)di * BN + rank * (BN / 2)));
+            } else {
             mbar_arrive_expect_tx(full + stage, STAGE_TX);   // whole tiles: own + peers' slices
 #pragma unroll
             for (int l = 0; l < NL; ++l) {
@@ -344,6 +397,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, kb * KE, yb, b_mask);
               else tma_load_2d(db, &tmB, full + stage, kb * KE, yb);
             }
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -352,8 +406,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ===================================================== Stage I MMA issuer (elected lane)
+    constexpr uint32_t IDESC_P = make_idesc<MODE>(2 * BM, BN);   // pair: M = 256
     int stage = 0, buf = 0;
     uint32_t phase = 0, bphase = 0;
     const uint64_t a_desc0 = sdesc(smem_u32(sA));
@@ -386,7 +441,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                 a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
                                 IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
           } else {
-            if constexpr (KBYTES == 128)
+            if constexpr (PAIR)
+              tc_mma4_pair_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
+                                       IDESC_P, acc);
+            else if constexpr (KBYTES == 128)
               tc_mma4_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
                                   IDESC, acc);
             else
@@ -396,14 +454,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if ((DBG(2049)) == 2049) {     // diagnostics (no MMAs): plain arrive instead of commit
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + stage);
-        } else if constexpr (MC) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
+        } else if constexpr (PAIR) tc_commit_pair_mc_elect(empty + stage, (uint16_t)3);
+        else if constexpr (MC) tc_commit_mc_elect(empty + stage, (uint16_t)(a_mask | b_mask));
         else tc_commit_elect(empty + stage);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      tc_commit_elect(tfull + buf);
+      if constexpr (PAIR) tc_commit_pair_mc_elect(tfull + buf, (uint16_t)3);
+      else tc_commit_elect(tfull + buf);
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
     }
@@ -416,7 +476,21 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       uint32_t cphase = 0;
       for (int64_t t = t0; t < t1; ++t) {
         const int di = (int)(t % p.TdG) * CLD + rd;
-        mbar_wait(cempty + cs, cphase ^ 1);
+        TWAIT(14, cempty + cs, cphase ^ 1);
+        if constexpr (PAIR) {
+          // this CTA's half of the class rows of each C part ([part][Kp/2][BN]), both halves
+          // completing on the leader's barrier; rows of 128 B in the tmC view of Cil
+          const uint32_t cbar = mapa_u32(cfull + cs, 0);
+          const int half = (int)(p.Kp * BN);            // bytes of Kp/2 rows x BN bf16
+          if (leader) mbar_arrive_expect_tx(cfull + cs, 2 * 2 * half);
+#pragma unroll
+          for (int part = 0; part < 2; ++part)
+            tma_load_2d_pair(sC + cs * CF::C_SLOT + part * half, &tmC, cbar, 0,
+                             (int)(((int64_t)di * c_tile_bytes + part * 2 * half + rank * half) / 128));
+          cs ^= 1;
+          if (cs == 0) cphase ^= 1;
+          continue;
+        }
         mbar_arrive_expect_tx(cfull + cs, (ENC ? 0u : c_tile_bytes) + (MODE == 2 ? BN * 8 : 0));
         if (!ENC)
           bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
@@ -428,7 +502,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
     }
     }
-  } else if (warp == 3) {
+  } else if (warp == 3 && leader) {
     if (!ENC && !(DBG(8192))) {
     // ===================================================== Stage II MMA issuer (elected lane)
     // A warp of its own: S += H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
@@ -436,8 +510,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int hb = 0, cs = 0;
     uint32_t hphase = 0, cphase = 0, sphase = 0;
     bool seg_first = true;
-    const uint32_t IDESC2 = make_idesc<0>(BM, (int)p.Kp);
+    const uint32_t IDESC2 = make_idesc<0>(PAIR ? 2 * BM : BM, (int)p.Kp);
     const uint32_t d2 = tmem_base + CF::D2_COL;
+    const uint32_t part_bytes = PAIR ? (uint32_t)(p.Kp * BN) : (uint32_t)(p.Kp * BN * 2);   // pair: half the classes
     for (int64_t t = t0; t < t1; ++t) {
       TWAIT(3, hfull + hb, hphase);
       TWAIT(4, cfull + cs, cphase);
@@ -450,9 +525,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
         for (int part = 0; part < 2; ++part) {      // C = hi + lo, both into the same columns
           const uint64_t bd = smem_desc_interleaved(
-              c_base + part * (uint32_t)(p.Kp * BN * 2) + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
+              c_base + part * part_bytes + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
           if (DBG(8)) continue;
-          if constexpr (CF::H_TMEM) {
+          if constexpr (PAIR) {
+            tc_mma_ts_pair_elect(d2, tmem_base + CF::H_COL + hb * (BN / 2) + s * 8, bd, IDESC2,
+                                 part == 0 ? acc : 1u);
+          } else if constexpr (CF::H_TMEM) {
             // A = H from TMEM (16 bf16 = 8 columns per k-step)
             tc_mma_ts_elect(d2, tmem_base + CF::H_COL + hb * (BN / 2) + s * 8, bd, IDESC2,
                             part == 0 ? acc : 1u);
@@ -464,10 +542,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
       }
       seg_first = false;
-      tc_commit_elect(hempty + hb);
-      tc_commit_elect(cempty + cs);
+      if constexpr (PAIR) {
+        tc_commit_pair_mc_elect(hempty + hb, (uint16_t)3);
+        tc_commit_pair_mc_elect(cempty + cs, (uint16_t)3);
+      } else {
+        tc_commit_elect(hempty + hb);
+        tc_commit_elect(cempty + cs);
+      }
       if (seg_last(t, t1, p.TdG)) {
-        tc_commit_elect(sfull);
+        if constexpr (PAIR) tc_commit_pair_mc_elect(sfull, (uint16_t)3);
+        else tc_commit_elect(sfull);
         seg_first = true;
         sphase ^= 1;
       }
@@ -565,7 +649,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(tempty + buf);                // accumulator free for tile t + 2
+        arrive_lead(tempty + buf);                // accumulator free for tile t + 2
         if (MODE == 2 && ENC) mbar_arrive(cempty + cs);   // encode mode: taus read
       }
       // H buffer hb free (Stage II of tile t - 2 done)
@@ -677,7 +761,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && !ENC) mbar_arrive(hfull + hb);
+      if (lane == 0 && !ENC) arrive_lead(hfull + hb);
       buf ^= 1;
       if (buf == 0) bphase ^= 1;
       if (++hb == NH) {
@@ -726,7 +810,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(sempty);
+        if (lane == 0) arrive_lead(sempty);
         if (sole && row_ok && p.labels) p.labels[row] = best;
         if (!sole) __threadfence();
       }
@@ -741,23 +825,38 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       named_bar(1, NUM_EPI * 32);
       if (*s_flag && cq == 0 && row_ok) {
         __threadfence();
+        // KC classes at a time, their partial loads independent (in flight together);
+        // per class the sum order is fixed: cluster, then D rank (bit-deterministic)
+        constexpr int KC = 16;
         int best = 0;
         float bv = 0.f;
-        for (int k = 0; k < K; ++k) {
-          float s = 0.f;
-          for (int cc = c_first; cc <= c_last; ++cc) {        // fixed order: cluster, then D rank
+        for (int k0 = 0; k0 < K; k0 += KC) {
+          float acc[KC];
+          bool first = true;
+          for (int cc = c_first; cc <= c_last; ++cc) {
             const int ng0 = (int)(range_begin(cc, p.T, p.G) / p.TdG);
             const int slot = (CLD == 1) ? ((ng0 == ng) ? 0 : 1) : (ng - ng0);
             for (int j = 0; j < CLD; ++j) {
               const int64_t cta = (int64_t)cc * CLS + rn * CLD + j;
-              const float v = ld_cg(p.S_part + ((cta * p.nslot + slot) * BM + m) * p.K + k);
-              s = (cc == c_first && j == 0) ? v : s + v;
+              const float* src = p.S_part + ((cta * p.nslot + slot) * BM + m) * p.K + k0;
+              float v[KC];
+#pragma unroll
+              for (int u = 0; u < KC; ++u) v[u] = (k0 + u < K) ? ld_cg(src + u) : 0.f;
+#pragma unroll
+              for (int u = 0; u < KC; ++u) acc[u] = first ? v[u] : acc[u] + v[u];
+              first = false;
             }
           }
-          if (p.scores) p.scores[row * p.K + k] = s;
-          if (k == 0 || s > bv) {
-            bv = s;
-            best = k;
+#pragma unroll
+          for (int u = 0; u < KC; ++u) {
+            const int k = k0 + u;
+            if (k < K) {
+              if (p.scores) p.scores[row * p.K + k] = acc[u];
+              if (k == 0 || acc[u] > bv) {
+                bv = acc[u];
+                best = k;
+              }
+            }
           }
         }
         if (p.labels) p.labels[row] = best;
@@ -777,7 +876,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -979,12 +1079,12 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC = true>
-cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p, int num_sms,
-                        cudaStream_t st) {
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC = true, bool PAIR = false>
+cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, TcParams& p,
+                        int num_sms, cudaStream_t st) {
   constexpr int CLS = CLN * CLD;
   const size_t sm = Cfg<MODE, BN>::TOTAL + 1024;
-  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC, HWC>;
+  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC, HWC, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1016,31 +1116,36 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, TcParams& p,
   p.nslot = (CLD == 1) ? 2 : (int)((per + p.TdG - 1) / p.TdG + 1);
   if ((int64_t)p.G * CLS * p.nslot > p.s_part_cap) return cudaErrorInvalidValue;   // workspace bound
   cfg.gridDim = dim3(p.G * CLS, 1, 1);
-  e = cudaLaunchKernelEx(&cfg, kern, a, b, (const TcParams)p);
+  e = cudaLaunchKernelEx(&cfg, kern, a, b, c, (const TcParams)p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int MODE, int BN, bool ENC>
 cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
-                             TcParams& p, int num_sms, cudaStream_t st) {
+                             const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
+  if constexpr (MODE != 2 && !ENC) {
+    if (virt == 2 && cl_n == 2 && cl_d == 1)   // CTA pair as one cta_group::2 MMA unit
+      return launch_mode<MODE, BN, 2, 1, false, true, true>(a, b, c, p, num_sms, st);
+  }
+  if (virt == 2) virt = 0;                      // pair requested where it does not apply: 2x1 cluster
   if (virt) {
-    if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false>(a, b, p, num_sms, st);
-    if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false>(a, b, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false>(a, b, c, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false>(a, b, c, p, num_sms, st);
     return cudaErrorInvalidValue;
   }
-  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC>(a, b, p, num_sms, st);
-  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC>(a, b, p, num_sms, st);
-  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC>(a, b, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC>(a, b, c, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC>(a, b, c, p, num_sms, st);
+  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC>(a, b, c, p, num_sms, st);
   return cudaErrorInvalidValue;
 }
 // ENC (encode mode, hdc_model_encode) is a separate instantiation so the inference kernel
 // carries no encode branches.
 template <int MODE, int BN>
 cudaError_t launch_cluster(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
-                           TcParams& p, int num_sms, cudaStream_t st) {
-  return p.hout ? launch_cluster_e<MODE, BN, true>(cl_n, cl_d, virt, a, b, p, num_sms, st)
-                : launch_cluster_e<MODE, BN, false>(cl_n, cl_d, virt, a, b, p, num_sms, st);
+                           const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
+  return p.hout ? launch_cluster_e<MODE, BN, true>(cl_n, cl_d, virt, a, b, c, p, num_sms, st)
+                : launch_cluster_e<MODE, BN, false>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
 }
 
 }  // namespace
@@ -1079,6 +1184,8 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
     if (got >= 2 && !(bn == 80 && mode != 2)) {
       if (got == 3 && vc == 'v' && en == 1 && (ed == 4 || ed == 8)) {
         n = 1; d = ed; v = 1;
+      } else if (got == 3 && vc == 'p' && en == 2 && ed == 1) {
+        n = 2; d = 1; v = 2;                      // CTA pair (cta_group::2)
       } else if (got == 2 && ((en == 1 && (ed == 1 || ed == 2)) || (en == 2 && ed == 1))) {
         n = en; d = ed; v = 0;
       }
@@ -1212,29 +1319,52 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
     cudaMemsetAsync(dbg_buf, 0, (16 + 512) * sizeof(unsigned long long), st);
     p.dbg = dbg_buf;
   }
+  static unsigned long long* wd_host = nullptr;   // watchdog records, host-mapped
+  if (p.debug & 16384) {
+    if (!wd_host) cudaHostAlloc((void**)&wd_host, (8 + 4 * 64) * sizeof(unsigned long long), cudaHostAllocMapped);
+    memset(wd_host, 0, (8 + 4 * 64) * sizeof(unsigned long long));
+    cudaHostGetDevicePointer((void**)&p.dbg, wd_host, 0);
+  }
   const int nl = (mode == 2) ? 3 : 1;
   const int esz = (mode == 0) ? 2 : (mode == 1) ? 4 : 1;
   const CUtensorMapDataType dt = (mode == 0)   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   const uint32_t kbytes = (mode == 2) ? 64 : HDC_TC_KB16;
   const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
-  const int a_rows = o.cl_virt ? BM : BM / o.cl_d, b_rows = o.cl_virt ? bn : bn / o.cl_n;
+  const int a_rows = o.cl_virt == 1 ? BM : BM / o.cl_d, b_rows = o.cl_virt == 1 ? bn : bn / o.cl_n;
   if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, a_rows, swz) ||
       !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, b_rows, swz))
     return cudaErrorInvalidValue;
+  // CTA-pair mode: each CTA loads half the class rows of a C tile part (rows of 128 B)
+  memset(&mc, 0, sizeof(mc));
+  if (o.cl_virt == 2 && o.Cil &&
+      !make_map_2d(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, o.Cil, 128,
+                   (uint64_t)(Td * (int64_t)p.c_tile_bytes / 128), 128, (uint32_t)(p.Kp * bn / 128),
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
   cudaError_t e;
-  if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
-  else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
-  else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, p, num_sms, st);
+  if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
+  else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
+  else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
   else if (o.cl_n == 1 && o.cl_d == 1)
-    e = (mode == 0) ? (p.hout ? launch_mode<0, 80, 1, 1, true>(ma, mb, p, num_sms, st)
-                              : launch_mode<0, 80, 1, 1, false>(ma, mb, p, num_sms, st))
-                    : (p.hout ? launch_mode<1, 80, 1, 1, true>(ma, mb, p, num_sms, st)
-                              : launch_mode<1, 80, 1, 1, false>(ma, mb, p, num_sms, st));
+    e = (mode == 0) ? (p.hout ? launch_mode<0, 80, 1, 1, true>(ma, mb, mc, p, num_sms, st)
+                              : launch_mode<0, 80, 1, 1, false>(ma, mb, mc, p, num_sms, st))
+                    : (p.hout ? launch_mode<1, 80, 1, 1, true>(ma, mb, mc, p, num_sms, st)
+                              : launch_mode<1, 80, 1, 1, false>(ma, mb, mc, p, num_sms, st));
   else e = cudaErrorInvalidValue;
+  if (e == cudaSuccess && (p.debug & 16384)) {
+    cudaStreamSynchronize(st);
+    const unsigned long long n = wd_host[1] < 64 ? wd_host[1] : 64;
+    fprintf(stderr, "[hdc tc watchdog] %s: %llu stalled waits\n", wd_host[0] ? "ABORTED" : "ok", wd_host[1]);
+    for (unsigned long long i = 0; i < n; ++i) {
+      const unsigned long long* r = wd_host + 8 + 4 * i;
+      fprintf(stderr, "  slot %2llu  cta %4llu  warp %2llu  parity %llu  since %llu kcyc\n", r[0], r[1], r[2],
+              r[3] >> 32, r[3] & 0xffffffffull);
+    }
+  }
   if (e == cudaSuccess && (p.debug & 1024)) {
     unsigned long long h[512];
     cudaStreamSynchronize(st);
@@ -1249,7 +1379,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
     cudaMemcpy(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost);
     const char* names[16] = {"prod.empty", "mma.tempty", "mma.full", "s2.hfull", "s2.cfull",
                              "s2.sempty", "epi.tfull", "epi.hempty", "epi.sfull", "prod.total",
-                             "mma.total", "cprod.total", "epi.total", "s2.total", "-", "epi.cfull"};
+                             "mma.total", "cprod.total", "epi.total", "s2.total", "cprod.cempty", "epi.cfull"};
     fprintf(stderr, "[hdc tc debug] mode %d, %d CTAs, %lld tiles; mean cycles per CTA:", mode, p.G,
             (long long)p.T);
     for (int i = 0; i < 16; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)h[i] / p.G);

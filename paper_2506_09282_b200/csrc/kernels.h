@@ -65,7 +65,7 @@ cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, cons
 struct TcOperands {
   int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to cl_d D-tiles; N_p to cl_n x 128 rows
   int cl_n, cl_d;                    // thread-block cluster shape (N-tiles x D-tiles), multicast
-  int cl_virt;                       // 1: virtual 1 x cl_d group (no hardware cluster / multicast)
+  int cl_virt;                       // 1: virtual 1 x cl_d group (no hardware cluster / multicast); 2: CTA pair (cta_group::2)
   const void* A;                     // [NL][N_p][Fp] staged X (limbs / rounded copy)
   const void* B;                     // [NL][Dq][Fp]  B^T (limbs / rounded copy), K-major
   const void* Cil;                   // per D-tile Stage II operand (tc_c_tile_bytes each)

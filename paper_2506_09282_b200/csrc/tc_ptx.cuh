@@ -135,6 +135,31 @@ __device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* desc,
 }
 
 // ---------------------------------------------------------------- clusters
+// shared::cluster address of the same variable in CTA `cta` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+  return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly in a peer CTA)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+// 2-D TMA load into this CTA's shared memory whose completion is counted on the
+// mbarrier at `bar_cluster` (shared::cluster address; the pair leader's barrier).
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* desc, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(desc), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -167,6 +192,19 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* smem_slot) {  // whole warp
                "n"(NCOLS)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_slot) {  // warp 1 of both CTAs of a pair
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_slot)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS)
+               : "memory");
 }
 template <int NCOLS>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp
@@ -287,6 +325,44 @@ __device__ __forceinline__ void tc_mma_i8x3_elect(uint32_t d0, uint64_t a0, uint
       "@e tcgen05.mma.cta_group::1.kind::i8 [d1], %2, %4, %6, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [d2], %3, %4, %9, 1;\n\t}" ::"r"(d0),
       "l"(a0), "l"(a1), "l"(a2), "l"(b), "r"(i240), "r"(i160), "r"(dcol), "r"(accumulate), "r"(i80)
+      : "memory");
+}
+
+// CTA-pair (cta_group::2, M = 256) forms, issued by the leader CTA only: A rows 0-127
+// from the leader's shared memory / TMEM lanes, 128-255 from the peer's; B's N extent
+// split, the first half from the leader, the second from the peer (same offsets).
+template <int KIND>
+__device__ __forceinline__ void tc_mma4_pair_elect(uint32_t d, uint64_t a0, uint64_t b0, uint64_t a1, uint64_t b1,
+                                                   uint64_t a2, uint64_t b2, uint64_t a3, uint64_t b3,
+                                                   uint32_t idesc, uint32_t accumulate) {
+#define HDC_MMA4P(KS)                                                                         \
+  asm volatile(                                                                             \
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %10, 0;\n\t"   \
+      "@e tcgen05.mma.cta_group::2." KS " [%0], %1, %2, %9, p;\n\t"                           \
+      "@e tcgen05.mma.cta_group::2." KS " [%0], %3, %4, %9, 1;\n\t"                           \
+      "@e tcgen05.mma.cta_group::2." KS " [%0], %5, %6, %9, 1;\n\t"                           \
+      "@e tcgen05.mma.cta_group::2." KS " [%0], %7, %8, %9, 1;\n\t}" ::"r"(d),                \
+      "l"(a0), "l"(b0), "l"(a1), "l"(b1), "l"(a2), "l"(b2), "l"(a3), "l"(b3), "r"(idesc),      \
+      "r"(accumulate)                                                                          \
+      : "memory")
+  if constexpr (KIND == 0) HDC_MMA4P("kind::f16");
+  else HDC_MMA4P("kind::tf32");
+#undef HDC_MMA4P
+}
+__device__ __forceinline__ void tc_mma_ts_pair_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                                     uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 

@@ -89,3 +89,26 @@ def test_tc_cfg2_full_size(hdc, prec):
 @pytest.mark.parametrize("name", ["cfg4", "cfg5", "cfg5_d2000", "cfg5_d20000"])
 def test_tc_large_configs(hdc, prec, name):
     print(prec, name, _full_size(hdc, name, prec))
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("N,F,D,K", [(33, 7, 17, 2), (300, 561, 2000, 6), (640, 784, 801, 10),
+                                     (1000, 33, 1000, 3), (129, 64, 250, 32)])
+def test_tc_cta_pair_mode(hdc, monkeypatch, prec, N, F, D, K):
+    # CTA pair (cta_group::2, M = 256, HDC_TC_CLUSTER=2x1p) must give the same labels and
+    # scores as the default 2x1 cluster: same operands, same per-element fp32 sums
+    rng = np.random.default_rng(N * 7 + F + D * 3 + K)
+    X = rng.uniform(-1, 1, (N, F)).astype(np.float32)
+    B = rng.standard_normal((F, D)).astype(np.float32)
+    C = rng.standard_normal((K, D)).astype(np.float32)
+    Bd, Cd = to_dev(B, C)
+    out = {}
+    for shape in ("2x1", "2x1p"):
+        monkeypatch.setenv("HDC_TC_CLUSTER", shape)
+        m = hdc.Model(Bd, Cd, prec=prec)
+        out[shape] = run_model(m, X, "fused")
+        m.close()
+    rep = check_lowp(oracle.infer(X, B, C), *out["2x1p"], rtol=max(1e-2, 32.0 / D))
+    print(prec, (N, F, D, K), rep)
+    assert np.array_equal(out["2x1"][0], out["2x1p"][0])
+    np.testing.assert_allclose(out["2x1"][1], out["2x1p"][1], rtol=1e-5, atol=1e-4)

@@ -21,7 +21,7 @@ def main():
     precs = os.environ.get("PRECS", "fp32_tc,bf16").split(",")
     flags = [int(f) for f in os.environ.get("FLAGS", "0,8,32,1,2,16,9").split(",")]
     dev = torch.device("cuda:0")
-    X = make_X_device(cfg, dev, 0, cfg.N)
+    X = make_X_device(cfg, dev, 0, int(os.environ.get("NROWS", cfg.N)))
     B = torch.from_numpy(make_B(cfg)).to(dev)
     C = torch.from_numpy(make_C(cfg)).to(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
