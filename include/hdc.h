@@ -108,14 +108,19 @@ hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int3
                                   float* scores, hdc_path_t path, void* stream);
 
 /* End-to-end variant on HOST buffers: copies X_host (N*F fp32) to the device,
- * runs hdc_model_infer, copies labels (and scores if non-NULL) back.  For N > 32
- * the rows are processed in up to 8 chunks of ~4096 whose host-to-device copies
- * run on a library-owned copy stream, overlapping the inference of the previous
- * chunk (rows are independent, so results equal the one-shot call).
+ * runs hdc_model_infer, copies labels (and scores if non-NULL) back.  The
+ * host-to-device copies run on a library-owned copy stream into one of two
+ * staging buffers, so back-to-back calls pipeline: the copy of call i + 1 overlaps
+ * the inference of call i.  For N > 32 the rows are also processed in up to 8
+ * chunks of ~8192, the copy of chunk j + 1 overlapping the inference of chunk j
+ * (rows are independent, so results equal the one-shot call).
+ * Ordering: the copies of X_host are ordered after this model's previous host-path
+ * calls, NOT after other work already queued on `stream` -- X_host must be fully
+ * written when the call is made.  Labels / scores are written in `stream` order.
  * Host buffers should be pinned (cudaHostAlloc) for the copies to be
  * asynchronous; the call returns after enqueue -- synchronise `stream` before
- * reading them.  Concurrent host-path calls on the same model must be serialised
- * by the caller (they share the model's staging buffers and copy stream). */
+ * reading the outputs or reusing X_host.  Concurrent host-path calls on the same
+ * model must be serialised by the caller (they share the staging buffers). */
 hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                                   int32_t* labels_host, float* scores_host, void* stream);
 

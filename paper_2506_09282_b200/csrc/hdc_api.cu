@@ -91,12 +91,13 @@ struct hdc_model_s {
   float* S_part_f = nullptr;
   unsigned* cnt_f = nullptr;
   // host-buffer (e2e) staging, grown on demand
-  float* Xdev = nullptr;
+  float* Xdev = nullptr;          // host-buffer path: two staging buffers of Xdev_rows x F
   int64_t Xdev_rows = 0;
+  int xbuf = 0;                   // staging buffer of the next call
+  cudaEvent_t ev_done[2] = {};    // compute that last read staging buffer b
   int32_t* ldev = nullptr;
   float* sdev = nullptr;
   cudaStream_t copy_stream = nullptr;   // host-buffer path: H2D copies, overlapped with compute
-  cudaEvent_t ev_start = nullptr;
   cudaEvent_t ev_h2d[8] = {};
   int32_t last_launches = 0;
   // diagnostics: CUDA events around the dominant kernel of each call
@@ -141,7 +142,8 @@ hdc_status_t check_dims(int64_t F, int64_t D, int64_t K) {
 
 void free_model_memory(hdc_model_s* m) {
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
-  if (m->ev_start) cudaEventDestroy(m->ev_start);
+  for (int i = 0; i < 2; ++i)
+    if (m->ev_done[i]) cudaEventDestroy(m->ev_done[i]);
   for (int i = 0; i < kHostChunksMax; ++i)
     if (m->ev_h2d[i]) cudaEventDestroy(m->ev_h2d[i]);
   if (m->ev0) cudaEventDestroy(m->ev0);
@@ -550,7 +552,7 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
   if (N == 0) return HDC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (N > m->Xdev_rows) {
-    cudaStreamSynchronize(s);
+    cudaDeviceSynchronize();                 // earlier calls may still read the staging buffers
     cudaFree(m->Xdev);
     cudaFree(m->ldev);
     cudaFree(m->sdev);
@@ -558,7 +560,7 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
     m->ldev = nullptr;
     m->sdev = nullptr;
     m->Xdev_rows = 0;
-    cudaError_t e = cudaMalloc((void**)&m->Xdev, sizeof(float) * N * m->F);
+    cudaError_t e = cudaMalloc((void**)&m->Xdev, sizeof(float) * 2 * N * m->F);
     if (e == cudaSuccess) e = cudaMalloc((void**)&m->ldev, sizeof(int32_t) * N);
     if (e == cudaSuccess) e = cudaMalloc((void**)&m->sdev, sizeof(float) * N * m->K);
     if (e != cudaSuccess) {
@@ -568,36 +570,45 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
     m->Xdev_rows = N;
   }
   if (!m->copy_stream) {
-    if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
       return fail(HDC_ERR_CUDA, "copy stream / event creation");
     for (int i = 0; i < kHostChunksMax; ++i)
       if (cudaEventCreateWithFlags(&m->ev_h2d[i], cudaEventDisableTiming) != cudaSuccess)
         return fail(HDC_ERR_CUDA, "event creation");
+    for (int i = 0; i < 2; ++i)
+      if (cudaEventCreateWithFlags(&m->ev_done[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(HDC_ERR_CUDA, "event creation");
   }
-  // Pipelined: the H2D copy of chunk i + 1 (copy stream) overlaps the inference of chunk i
-  // (caller's stream); labels (and scores) come back per chunk.  Rows are independent
-  // (Alg. 1 per sample), so chunking changes nothing in the results.
+  // Pipelined, two ways.  (1) Across calls: X goes to one of two staging buffers, so
+  // the copy of call i + 1 needs only the compute of call i - 1 (which read that
+  // buffer) to be done, and overlaps the compute of call i.  (2) Within a call: chunks,
+  // the copy of chunk j + 1 overlapping the inference of chunk j.  Copies run on the
+  // model's copy stream in call order; compute and the label copies on `stream`.
+  // Rows are independent (Alg. 1 per sample), so chunking changes nothing in the results.
   int nchunks = 1;
   if (N > kSmallMaxN) {
     const char* ev = getenv("HDC_HOST_CHUNK_ROWS");   // diagnostics override
-    const int64_t target = ev ? atoll(ev) : 4096;     // rows per chunk (>= one full wave of tiles)
+    const int64_t target = ev ? atoll(ev) : 8192;     // rows per chunk (>= a few waves of tiles)
     nchunks = (int)((N + target - 1) / target);
     if (nchunks > kHostChunksMax) nchunks = kHostChunksMax;
   }
   const int64_t per = (N + nchunks - 1) / nchunks;
-  HDC_CUDA_TRY(cudaEventRecord(m->ev_start, s), "event record");
-  HDC_CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->ev_start, 0), "stream wait");
+  const int b = m->xbuf;
+  m->xbuf ^= 1;
+  float* xd = m->Xdev + (int64_t)b * m->Xdev_rows * m->F;
+  HDC_CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->ev_done[b], 0), "stream wait");
+  // (same stream: a no-op; another stream: the device labels / scores are not reused early)
+  HDC_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_done[b ^ 1], 0), "stream wait");
   int32_t launches = 0;
   for (int i = 0; i < nchunks; ++i) {
     const int64_t r0 = i * per, n = (r0 + per <= N) ? per : N - r0;
     if (n <= 0) break;
-    HDC_CUDA_TRY(cudaMemcpyAsync(m->Xdev + r0 * m->F, X_host + r0 * m->F, sizeof(float) * n * m->F,
+    HDC_CUDA_TRY(cudaMemcpyAsync(xd + r0 * m->F, X_host + r0 * m->F, sizeof(float) * n * m->F,
                                  cudaMemcpyHostToDevice, m->copy_stream),
                  "H2D X");
     HDC_CUDA_TRY(cudaEventRecord(m->ev_h2d[i], m->copy_stream), "event record");
     HDC_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_h2d[i], 0), "stream wait");
-    st = run(m, m->Xdev + r0 * m->F, n, m->ldev + r0, scores_host ? m->sdev + r0 * m->K : nullptr,
+    st = run(m, xd + r0 * m->F, n, m->ldev + r0, scores_host ? m->sdev + r0 * m->K : nullptr,
              HDC_PATH_AUTO, s);
     if (st != HDC_OK) return st;
     launches += m->last_launches;
@@ -608,6 +619,7 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                                    cudaMemcpyDeviceToHost, s),
                    "D2H scores");
   }
+  HDC_CUDA_TRY(cudaEventRecord(m->ev_done[b], s), "event record");
   m->last_launches = launches;
   return HDC_OK;
 }

@@ -132,3 +132,34 @@ def test_argmax_ties_lowest_index(hdc):
     S2[:, 7] = S2.max(dim=1).values
     S2[:, 250] = S2[:, 7]
     assert np.array_equal(hdc.argmax(S2).cpu().numpy(), np.argmax(S2.cpu().numpy(), axis=1))
+
+
+@pytest.mark.parametrize("prec", ["fp32_tc", "bf16"])
+def test_host_path_pipelined_calls(hdc, prec):
+    # back-to-back host-buffer calls share two staging buffers and overlap the copy of
+    # call i + 1 with the compute of call i; every call's labels / scores must equal the
+    # device-resident call on the same rows (chunked: N > 8192; growing N reallocates;
+    # a call on another stream must not race the previous call's outputs)
+    rng = np.random.default_rng(5)
+    F, D, K = 97, 3000, 7
+    B = rng.standard_normal((F, D)).astype(np.float32)
+    C = rng.standard_normal((K, D)).astype(np.float32)
+    Bd, Cd = to_dev(B, C)
+    m = hdc.Model(Bd, Cd, prec=prec)
+    sizes = [5000, 20000, 20000, 33, 20000, 30000, 7]
+    Xs = [rng.uniform(-1, 1, (n, F)).astype(np.float32) for n in sizes]
+    hosts = [(torch.from_numpy(X).pin_memory(), torch.empty(X.shape[0], dtype=torch.int32).pin_memory(),
+              torch.empty(X.shape[0], K, dtype=torch.float32).pin_memory()) for X in Xs]
+    side = torch.cuda.Stream()
+    for i, (Xh, yh, Sh) in enumerate(hosts):
+        m.infer_host(Xh, yh, Sh, stream=side if i == 4 else None)
+    torch.cuda.synchronize()
+    for X, (Xh, yh, Sh) in zip(Xs, hosts):
+        y, S = run_model(m, X, "auto")
+        # chunking changes how a row's D-range is split over CTAs, so the fp32 partial
+        # sums may round differently; labels must agree wherever the top-2 gap is clear
+        np.testing.assert_allclose(Sh.numpy(), S, rtol=1e-5, atol=1e-3)
+        top2 = np.sort(S, axis=1)[:, -2:]
+        clear = (top2[:, 1] - top2[:, 0]) > 1e-2
+        assert np.array_equal(yh.numpy()[clear], y[clear])
+    m.close()

@@ -65,9 +65,45 @@ def main():
     for rows in (2048, 4096, 8192, 16384):
         os.environ["HDC_HOST_CHUNK_ROWS"] = str(rows)
         ms = timed(lambda: m.infer_host(Xh, yh))
-        print("infer_host chunk=%6d: %.3f ms per step  %.2f M samples/s" % (rows, ms, cfg.N / ms / 1e3))
+
+        def ten():
+            for _ in range(10):
+                m.infer_host(Xh, yh)
+        ms10 = timed(ten, reps=3) / 10
+        print("infer_host chunk=%6d: %.3f ms one call, %.3f ms per call back-to-back (%.2f M samples/s)"
+              % (rows, ms, ms10, cfg.N / ms10 / 1e3))
     m.close()
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("BENCH_LIKE"):
     main()
+
+
+def bench_like():
+    """The bench.py e2e pattern: 2 warm-up calls, then 20 back-to-back calls, with
+    per-call events on the compute stream."""
+    cfg = CONFIGS[os.environ.get("CFG", "cfg2")]
+    dev = torch.device("cuda:0")
+    X = make_X_device(cfg, dev, 0, cfg.N)
+    m = hdc.Model(torch.from_numpy(make_B(cfg)).to(dev), torch.from_numpy(make_C(cfg)).to(dev),
+                  prec=os.environ.get("PREC", "fp32_tc"))
+    for _ in range(3):
+        m.infer(X)
+    Xh = X.cpu().pin_memory()
+    yh = torch.empty(cfg.N, dtype=torch.int32).pin_memory()
+    for _ in range(2):
+        m.infer_host(Xh, yh)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(21)]
+    ev[0].record()
+    for i in range(20):
+        m.infer_host(Xh, yh)
+        ev[i + 1].record()
+    torch.cuda.synchronize()
+    d = [ev[i].elapsed_time(ev[i + 1]) for i in range(20)]
+    print("bench-like per call ms:", " ".join("%.3f" % x for x in d), " total %.3f" % ev[0].elapsed_time(ev[20]))
+    m.close()
+
+
+if __name__ == "__main__" and os.environ.get("BENCH_LIKE"):
+    bench_like()

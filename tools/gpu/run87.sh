@@ -1,0 +1,2 @@
+timeout 200 python tools/e2e_probe.py 2>&1 | grep infer_host
+PREC=bf16 timeout 200 python tools/e2e_probe.py 2>&1 | grep infer_host
