@@ -50,9 +50,12 @@ using namespace ptx;
 
 constexpr int BM = 128;              // rows per tile (MMA M)
 constexpr int STAGES_MAX = 6;
-// K bytes per operand stage for bf16/tf32 (int8 always 64): 64 B (SWIZZLE_64B) halves the
-// stage and doubles the ring depth, so the producer / MMA handshakes of more stages are
-// in flight (measured: each stage hand-off costs ~1 us of barrier latency round trip).
+// K bytes per operand stage (one swizzle-atom row).  Fewer, larger stages mean fewer
+// producer / MMA hand-offs: int8 at 128 B (2 stages of 78 KB) runs 5% faster than at
+// 64 B (4 stages of 39 KB) at cfg2; bf16/tf32 at 64 B was slower than at 128 B.
+#ifndef HDC_TC_KB8
+#define HDC_TC_KB8 128                               // int8 mode K bytes per stage (SWIZZLE_128B)
+#endif
 #ifndef HDC_TC_KB16
 #define HDC_TC_KB16 128
 #endif
@@ -80,9 +83,8 @@ struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int NL = (MODE == 2) ? 3 : 1;
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
-  // K bytes per stage = one swizzle-atom row: 128 B (SWIZZLE_128B) for the single-operand
-  // modes, 64 B (SWIZZLE_64B) for the 3-limb int8 mode (smem budget).
-  static constexpr int KBYTES = (MODE == 2) ? 64 : HDC_TC_KB16;
+  // K bytes per stage = one swizzle-atom row (HDC_TC_KB8 / HDC_TC_KB16).
+  static constexpr int KBYTES = (MODE == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
   static constexpr int SWZ = (KBYTES == 64) ? 4 : 2;             // descriptor layout type
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
   static constexpr int A_LIMB_BYTES = BM * KBYTES;
@@ -119,7 +121,7 @@ struct Cfg {
   static constexpr int OFF_C = OFF_H + H_REGION;
   static constexpr int OFF_BAR = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;
   static constexpr int TOTAL = OFF_BAR + 512;
-  static_assert(STAGES_ >= 3, "pipeline depth");
+  static_assert(STAGES_ >= (KBYTES == 128 && MODE == 2 ? 2 : 3), "pipeline depth");
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
   static_assert(C_SLOT % 16 == 0, "bulk-copy granule");
   static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
@@ -313,7 +315,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
   for (int i = 0; i < CLN; ++i) b_mask |= (uint16_t)(1u << (i * CLD + rd));
   const int64_t t0 = range_begin(cl, p.T, p.G), t1 = range_begin(cl + 1, p.T, p.G);
-  const int KB = (int)(p.Fp / KE);
+  // K stages; the int8 mode's 128-byte stages may overhang Fp (a multiple of 64) by 64
+  // elements: TMA zero-fills past the tensor's extent and the MMA skips those k-steps
+  const int KB = (int)((p.Fp + KE - 1) / KE);
+  const int last_ks = (int)(((p.Fp - (int64_t)(KB - 1) * KE) * CF::ESZ + 31) / 32);
   const bool leader = !PAIR || rank == 0;
   // pair mode: barriers the leader's MMA warps wait on are the leader's
   auto arrive_lead = [&](uint64_t* bar) {
@@ -435,8 +440,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             // the accumulators contiguous columns [A0 | A1 | A2], so one MMA per A limb:
             //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
             // (each A tile is read from shared memory once per k-step, not 3 times).
+            const int nks = (kb == KB - 1) ? last_ks : KBYTES / 32;
 #pragma unroll
             for (int ks = 0; ks < KBYTES / 32; ++ks)
+              if (ks < nks)
               tc_mma_i8x3_elect(acc0, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
                                 a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
                                 IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
@@ -1331,7 +1338,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUtensorMap ma, mb, mc;
-  const uint32_t kbytes = (mode == 2) ? 64 : HDC_TC_KB16;
+  const uint32_t kbytes = (mode == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
   const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
   const int a_rows = o.cl_virt == 1 ? BM : BM / o.cl_d, b_rows = o.cl_virt == 1 ? bn : bn / o.cl_n;
