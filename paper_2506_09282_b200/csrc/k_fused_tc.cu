@@ -56,6 +56,9 @@ constexpr int STAGES_MAX = 6;
 #ifndef HDC_TC_KB8
 #define HDC_TC_KB8 128                               // int8 mode K bytes per stage (SWIZZLE_128B)
 #endif
+#ifndef HDC_TC_NAT16
+#define HDC_TC_NAT16 1                               // bf16/tf32: swizzle atoms per stage
+#endif
 #ifndef HDC_TC_KB16
 #define HDC_TC_KB16 128
 #endif
@@ -87,9 +90,13 @@ struct Cfg {
   static constexpr int KBYTES = (MODE == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
   static constexpr int SWZ = (KBYTES == 64) ? 4 : 2;             // descriptor layout type
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
-  static constexpr int A_LIMB_BYTES = BM * KBYTES;
-  static constexpr int B_LIMB_BYTES = BN * KBYTES;
-  static constexpr int KE = KBYTES / ESZ;                        // K elements per stage
+  // bf16/tf32: NAT swizzle atoms (K blocks of KBYTES) per stage, each a [rows][KBYTES] tile
+  static constexpr int NAT = (MODE == 2) ? 1 : HDC_TC_NAT16;
+  static constexpr int ATOM_A = BM * KBYTES, ATOM_B = BN * KBYTES;
+  static constexpr int A_LIMB_BYTES = NAT * ATOM_A;
+  static constexpr int B_LIMB_BYTES = NAT * ATOM_B;
+  static constexpr int KA = KBYTES / ESZ;                        // K elements per atom
+  static constexpr int KE = NAT * KA;                            // K elements per stage
   static constexpr int KP_MAX = (MODE == 2 || BN > 80) ? KP_MAX_I8 : KP_MAX_16;
   // TMEM columns: two Stage I accumulator buffers, the Stage II accumulator (hi and lo C
   // parts accumulate into the same Kp columns) and, for bf16/tf32, two H tiles as the
@@ -121,7 +128,7 @@ struct Cfg {
   static constexpr int OFF_C = OFF_H + H_REGION;
   static constexpr int OFF_BAR = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;
   static constexpr int TOTAL = OFF_BAR + 512;
-  static_assert(STAGES_ >= (KBYTES == 128 && MODE == 2 ? 2 : 3), "pipeline depth");
+  static_assert(STAGES_ >= ((KBYTES == 128 && MODE == 2) || NAT > 1 ? 2 : 3), "pipeline depth");
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
   static_assert(C_SLOT % 16 == 0, "bulk-copy granule");
   static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
@@ -319,6 +326,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // elements: TMA zero-fills past the tensor's extent and the MMA skips those k-steps
   const int KB = (int)((p.Fp + KE - 1) / KE);
   const int last_ks = (int)(((p.Fp - (int64_t)(KB - 1) * KE) * CF::ESZ + 31) / 32);
+  const int last_at = (int)((p.Fp - (int64_t)(KB - 1) * KE + CF::KA - 1) / CF::KA);   // atoms used
   const bool leader = !PAIR || rank == 0;
   // pair mode: barriers the leader's MMA warps wait on are the leader's
   auto arrive_lead = [&](uint64_t* bar) {
@@ -385,22 +393,29 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               // both CTAs' loads complete on the leader's barrier (the leader's MMA waits on it)
               const uint32_t fbar = mapa_u32(full + stage, 0);
               // (the leader's own barrier: a CTA-scope arrive, no cluster-scope release fence)
-              if (leader) mbar_arrive_expect_tx(full + stage, 2 * (CF::A_LIMB_BYTES + (BN / 2) * KBYTES));
-              tma_load_2d_pair(sA + stage * CF::A_STAGE, &tmA, fbar, kb * KE, (int)((int64_t)ni * BM));
-              tma_load_2d_pair(sB + stage * CF::B_STAGE, &tmB, fbar, kb * KE,
-                               (int)((int64_t)di * BN + rank * (BN / 2)));
+              if (leader) mbar_arrive_expect_tx(full + stage, 2 * CF::NAT * (CF::ATOM_A + (BN / 2) * KBYTES));
+#pragma unroll
+              for (int a = 0; a < CF::NAT; ++a) {
+                tma_load_2d_pair(sA + stage * CF::A_STAGE + a * CF::ATOM_A, &tmA, fbar, kb * KE + a * CF::KA,
+                                 (int)((int64_t)ni * BM));
+                tma_load_2d_pair(sB + stage * CF::B_STAGE + a * CF::ATOM_B, &tmB, fbar, kb * KE + a * CF::KA,
+                                 (int)((int64_t)di * BN + rank * (BN / 2)));
+              }
             } else {
             mbar_arrive_expect_tx(full + stage, STAGE_TX);   // whole tiles: own + peers' slices
 #pragma unroll
-            for (int l = 0; l < NL; ++l) {
-              uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + ra * AR * KBYTES;
+            for (int l = 0; l < NL; ++l)
+#pragma unroll
+              for (int a = 0; a < CF::NAT; ++a) {
+              uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + a * CF::ATOM_A + ra * AR * KBYTES;
               const int ya = (int)(l * p.Np + (int64_t)ni * BM + ra * AR);
-              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + rb * BR * KBYTES;
+              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + a * CF::ATOM_B + rb * BR * KBYTES;
               const int yb = (int)(l * p.Dq + (int64_t)di * BN + rb * BR);
-              if constexpr (MC && CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, kb * KE, ya, a_mask);
-              else tma_load_2d(da, &tmA, full + stage, kb * KE, ya);
-              if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, kb * KE, yb, b_mask);
-              else tma_load_2d(db, &tmB, full + stage, kb * KE, yb);
+              const int xk = kb * KE + a * CF::KA;
+              if constexpr (MC && CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, xk, ya, a_mask);
+              else tma_load_2d(da, &tmA, full + stage, xk, ya);
+              if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, xk, yb, b_mask);
+              else tma_load_2d(db, &tmB, full + stage, xk, yb);
             }
             }
           }
@@ -448,14 +463,20 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                 a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
                                 IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
           } else {
-            if constexpr (PAIR)
-              tc_mma4_pair_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
-                                       IDESC_P, acc);
-            else if constexpr (KBYTES == 128)
-              tc_mma4_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6,
-                                  IDESC, acc);
-            else
-              tc_mma2_elect<MODE>(acc0, a_d, b_d, a_d + 2, b_d + 2, IDESC, acc);
+            const int nat = (kb == KB - 1) ? last_at : CF::NAT;
+#pragma unroll
+            for (int at = 0; at < CF::NAT; ++at) {
+              if (at >= nat) continue;
+              const uint64_t aa = a_d + (uint64_t)((at * CF::ATOM_A) >> 4);
+              const uint64_t bb = b_d + (uint64_t)((at * CF::ATOM_B) >> 4);
+              const uint32_t ac = at == 0 ? acc : 1u;
+              if constexpr (PAIR)
+                tc_mma4_pair_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, aa + 4, bb + 4, aa + 6, bb + 6, IDESC_P, ac);
+              else if constexpr (KBYTES == 128)
+                tc_mma4_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, aa + 4, bb + 4, aa + 6, bb + 6, IDESC, ac);
+              else
+                tc_mma2_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, IDESC, ac);
+            }
           }
         }
         if ((DBG(2049)) == 2049) {     // diagnostics (no MMAs): plain arrive instead of commit
