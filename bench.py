@@ -14,6 +14,7 @@ Prints ONE JSON line (rank 0).
 import argparse
 import json
 import os
+import re
 import subprocess
 import sys
 import threading
@@ -151,8 +152,10 @@ def measured_traffic(cfg_name, prec):
     --set full capture (profiles/**/traffic.json), else None."""
     import glob
     best = None
+    def natural(path):                   # profiles/roundN/vM: later rounds / versions last
+        return [int(t) if t.isdigit() else t for t in re.split(r"(\d+)", path)]
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "**", "traffic.json"), recursive=True),
-                    key=os.path.getmtime):
+                    key=natural):
         try:
             with open(f) as fh:
                 d = json.load(fh)

@@ -51,11 +51,9 @@ using namespace ptx;
 constexpr int BM = 128;              // rows per tile (MMA M)
 constexpr int STAGES_MAX = 6;
 // K bytes per operand stage (one swizzle-atom row).  Fewer, larger stages mean fewer
-// producer / MMA hand-offs: int8 at 128 B (2 stages of 78 KB) runs 5% faster than at
-// 64 B (4 stages of 39 KB) at cfg2; bf16/tf32 at 64 B was slower than at 128 B.
-#ifndef HDC_TC_KB8
-#define HDC_TC_KB8 128                               // int8 mode K bytes per stage (SWIZZLE_128B)
-#endif
+// producer / MMA hand-offs: int8 at 128 B (2 stages of 78 KB) runs 8% faster than at
+// 64 B (4 stages of 39 KB) at cfg2 (tc_kbytes); bf16/tf32 at 64 B was slower than 128 B.
+#define HDC_TC_KB8 64                                // int8 mode default (launch picks 64 / 128 by Fp)
 #ifndef HDC_TC_NAT16
 #define HDC_TC_NAT16 1                               // bf16/tf32: swizzle atoms per stage
 #endif
@@ -81,13 +79,13 @@ __host__ __device__ constexpr int tile_n_for(int mode, int64_t K) {
   return (mode == 2) ? 80 : (K <= 32 ? 160 : 80);
 }
 
-template <int MODE, int BN_>
+template <int MODE, int BN_, int KW = 0>
 struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int NL = (MODE == 2) ? 3 : 1;
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
   // K bytes per stage = one swizzle-atom row (HDC_TC_KB8 / HDC_TC_KB16).
-  static constexpr int KBYTES = (MODE == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
+  static constexpr int KBYTES = KW ? KW : (MODE == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
   static constexpr int SWZ = (KBYTES == 64) ? 4 : 2;             // descriptor layout type
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
   // bf16/tf32: NAT swizzle atoms (K blocks of KBYTES) per stage, each a [rows][KBYTES] tile
@@ -254,11 +252,11 @@ __device__ __forceinline__ bool seg_last(int64_t t, int64_t t1, int Td) {
   return (t + 1 == t1) || ((t + 1) / Td != t / Td);
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC, bool PAIR>
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC, bool PAIR, int KW>
 __global__ void __launch_bounds__(THREADS, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const TcParams p) {
-  using CF = Cfg<MODE, BN>;
+  using CF = Cfg<MODE, BN, KW>;
   // PAIR: the 2 CTAs of a cluster run as one cta_group::2 MMA unit (M = 256: N-tiles
   // 2ng, 2ng+1; each CTA holds its 128 X rows and HALF of the B tile and of the C tile in
   // its own shared memory, so each SM ingests 128 + BN/2 operand rows per k-step instead of
@@ -1107,12 +1105,12 @@ bool make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* ba
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC = true, bool PAIR = false>
+template <int MODE, int BN, int CLN, int CLD, bool ENC, bool HWC = true, bool PAIR = false, int KW = 0>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, TcParams& p,
                         int num_sms, cudaStream_t st) {
   constexpr int CLS = CLN * CLD;
-  const size_t sm = Cfg<MODE, BN>::TOTAL + 1024;
-  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC, HWC, PAIR>;
+  const size_t sm = Cfg<MODE, BN, KW>::TOTAL + 1024;
+  auto kern = fused_tc_kernel<MODE, BN, CLN, CLD, ENC, HWC, PAIR, KW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1149,8 +1147,8 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   return cudaGetLastError();
 }
 
-template <int MODE, int BN, bool ENC>
-cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
+template <int MODE, int BN, bool ENC, int KW>
+cudaError_t launch_cluster_k(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
                              const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
   if constexpr (MODE != 2 && !ENC) {
     if (virt == 2 && cl_n == 2 && cl_d == 1)   // CTA pair as one cta_group::2 MMA unit
@@ -1158,14 +1156,29 @@ cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a,
   }
   if (virt == 2) virt = 0;                      // pair requested where it does not apply: 2x1 cluster
   if (virt) {
-    if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false>(a, b, c, p, num_sms, st);
-    if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false>(a, b, c, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false, false, KW>(a, b, c, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false, false, KW>(a, b, c, p, num_sms, st);
     return cudaErrorInvalidValue;
   }
-  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC>(a, b, c, p, num_sms, st);
-  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC>(a, b, c, p, num_sms, st);
-  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC>(a, b, c, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC, true, false, KW>(a, b, c, p, num_sms, st);
+  if (cl_n == 1 && cl_d == 2) return launch_mode<MODE, BN, 1, 2, ENC, true, false, KW>(a, b, c, p, num_sms, st);
+  if (cl_n == 2 && cl_d == 1) return launch_mode<MODE, BN, 2, 1, ENC, true, false, KW>(a, b, c, p, num_sms, st);
   return cudaErrorInvalidValue;
+}
+// int8 mode: 128-byte K stages when Fp is a multiple of 128 (half the producer / MMA
+// hand-offs), else 64-byte stages (a 128-byte last stage would load 64 bytes of zeros
+// per row: cfg4, F = 784, ran 7% slower)
+int tc_kbytes(int mode, int64_t Fp) { return mode == 2 ? ((Fp % 128 == 0) ? 128 : 64) : HDC_TC_KB16; }
+template <int MODE, int BN, bool ENC>
+cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
+                             const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
+  if constexpr (MODE == 2) {
+    if (tc_kbytes(MODE, p.Fp) == 128)
+      return launch_cluster_k<MODE, BN, ENC, 128>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
+    return launch_cluster_k<MODE, BN, ENC, 64>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
+  } else {
+    return launch_cluster_k<MODE, BN, ENC, 0>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
+  }
 }
 // ENC (encode mode, hdc_model_encode) is a separate instantiation so the inference kernel
 // carries no encode branches.
@@ -1359,7 +1372,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUtensorMap ma, mb, mc;
-  const uint32_t kbytes = (mode == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
+  const uint32_t kbytes = (uint32_t)tc_kbytes(mode, o.Fp);
   const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
   const int a_rows = o.cl_virt == 1 ? BM : BM / o.cl_d, b_rows = o.cl_virt == 1 ? bn : bn / o.cl_n;
