@@ -170,7 +170,12 @@ struct TcParams {
 #define HDC_I8_EPI_UNROLL 1
 #endif
 constexpr int kI8EpiUnroll = HDC_I8_EPI_UNROLL;
+#ifdef HDC_TC_DIAG_MASK
+// compile-time ablation (no runtime checks): DBG(m) is a constant
+#define DBG(mask) ((HDC_TC_DIAG_MASK) & (mask))
+#else
 #define DBG(mask) (HDC_TC_DIAG ? (p.debug & (mask)) : 0)
+#endif
 
 // Watchdog wait (diagnostics, debug & 16384): a wait that has not completed after ~1 s
 // records (slot, CTA, warp, parity) in the host-mapped p.dbg buffer and sets an abort
@@ -470,8 +475,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               const uint32_t ac = at == 0 ? acc : 1u;
               if constexpr (PAIR)
                 tc_mma4_pair_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, aa + 4, bb + 4, aa + 6, bb + 6, IDESC_P, ac);
-              else if constexpr (KBYTES == 128)
+              else if constexpr (KBYTES == 128) {
                 tc_mma4_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, aa + 4, bb + 4, aa + 6, bb + 6, IDESC, ac);
+                if (DBG(32768))   // diagnostics: twice the MMA work per stage (wrong results)
+                  tc_mma4_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, aa + 4, bb + 4, aa + 6, bb + 6, IDESC, 1u);
+              }
               else
                 tc_mma2_elect<MODE>(acc0, aa, bb, aa + 2, bb + 2, IDESC, ac);
             }

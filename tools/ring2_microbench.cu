@@ -6,9 +6,11 @@
 #include "../paper_2506_09282_b200/csrc/tc_ptx.cuh"
 using namespace hdc::ptx;
 
-template <int N, int VARIANT, bool RANDOM = false, int NT = 128>   // VARIANT 0: elect-issue (kernel), 1: lane-0 issue, 2: elect, fixed D,
+template <int N, int VARIANT, bool RANDOM = false, int NT = 128, int DELAY = 0>   // VARIANT 0: elect-issue (kernel), 1: lane-0 issue, 2: elect, fixed D,
                                                      // 3: no MMA (commit only), 4: no MMA, plain arrive
 __global__ void __launch_bounds__(NT, 1) ring2(int iters, unsigned long long* out) {
+  // DELAY: dependent integer ops the MMA warp executes per stage after its commit
+  // (probes how much per-stage issue work the tensor-core queue hides)
   constexpr int STAGES = 5, A_ST = 16384, B_ST = N * 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -52,6 +54,12 @@ __global__ void __launch_bounds__(NT, 1) ring2(int iters, unsigned long long* ou
       tc_fence_after();
       const uint32_t a = smem_u32(smem + s * A_ST), b = smem_u32(smem + STAGES * A_ST + s * B_ST);
       const uint32_t d = (VARIANT == 2) ? tb : tb + ((i / 10) & 1) * N;
+      if (VARIANT == 5) {   // the K4 kernel's form: base descriptor + offset, 4 MMAs under one elect
+        const uint64_t a_d = smem_desc_sw(smem_u32(smem), 1024, 2) + (uint64_t)((s * A_ST) >> 4);
+        const uint64_t b_d = smem_desc_sw(smem_u32(smem + STAGES * A_ST), 1024, 2) + (uint64_t)((s * B_ST) >> 4);
+        tc_mma4_elect<0>(d, a_d, b_d, a_d + 2, b_d + 2, a_d + 4, b_d + 4, a_d + 6, b_d + 6, idesc,
+                         (i % 10 == 0) ? 0u : 1u);
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (VARIANT >= 3) continue;
@@ -63,6 +71,12 @@ __global__ void __launch_bounds__(NT, 1) ring2(int iters, unsigned long long* ou
       if (VARIANT == 1) tc_commit(&empty[s]);
       else if (VARIANT == 4) { __syncwarp(); if (lane == 0) mbar_arrive(&empty[s]); }
       else tc_commit_elect(&empty[s]);
+      if (DELAY) {
+        uint32_t x = (uint32_t)i;
+#pragma unroll 1
+        for (int j = 0; j < DELAY; ++j) x = x * 1664525u + 1013904223u;
+        if (x == 0x12345678u) out[1000 + blockIdx.x] = x;
+      }
       if (++s == STAGES) { s = 0; ph ^= 1; }
     }
     if (VARIANT == 1) tc_commit(&done); else tc_commit_elect(&done);
@@ -77,12 +91,12 @@ __global__ void __launch_bounds__(NT, 1) ring2(int iters, unsigned long long* ou
   if (warp == 1) tmem_dealloc<512>(tb);
 }
 
-template <int N, int VARIANT, bool RANDOM = false, int NT = 128>
+template <int N, int VARIANT, bool RANDOM = false, int NT = 128, int DELAY = 0>
 void run(const char* name, int iters = 4000) {
   const int blocks = 148;
   unsigned long long* d;
   cudaMalloc(&d, sizeof(unsigned long long) * blocks * 2);
-  auto k = ring2<N, VARIANT, RANDOM, NT>;
+  auto k = ring2<N, VARIANT, RANDOM, NT, DELAY>;
   const int sm = 5 * (16384 + N * 128) + 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   k<<<blocks, NT, sm>>>(iters, d);
@@ -98,16 +112,13 @@ void run(const char* name, int iters = 4000) {
 }
 
 int main() {
-  run<160, 0>("N=160 elect, D alternating");
-  run<160, 1>("N=160 lane0, D alternating");
-  run<160, 2>("N=160 elect, D fixed");
-  run<80, 0>("N=80 elect, D alternating");
-  run<160, 3>("no MMA, commit per stage");
-  run<160, 3, false, 384>("no MMA, commit per stage, 384 threads");
-  run<160, 0, false, 384>("N=160 elect, 384 threads");
-  run<160, 4>("no MMA, plain arrive per stage");
-  run<160, 0, true>("N=160 elect, random data");
-  run<160, 0, false>("N=160 elect, zero data, long", 200000);
-  run<160, 0, true>("N=160 elect, random data, long", 200000);
+  run<160, 5>("N=160 K4-style mma4 (base+offset descriptors)");
+  run<160, 5, true>("N=160 K4-style mma4, random data");
+  run<160, 0>("N=160 elect, delay 0");
+  run<160, 0, false, 128, 16>("N=160 elect, delay 16 dep-ops/stage");
+  run<160, 0, false, 128, 32>("N=160 elect, delay 32 dep-ops/stage");
+  run<160, 0, false, 128, 64>("N=160 elect, delay 64 dep-ops/stage");
+  run<160, 0, false, 128, 128>("N=160 elect, delay 128 dep-ops/stage");
+  run<160, 3, false, 128, 64>("no MMA, delay 64 dep-ops/stage");
   return 0;
 }
