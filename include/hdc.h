@@ -74,8 +74,9 @@ typedef enum {
 } hdc_precision_t;
 
 /* Kernel selection (diagnostics and tests; HDC_PATH_AUTO is the product path).
- *   SMALL: bandwidth-bound D-split kernel (streams B and C once per 32 rows).
- *   FUSED: large-batch fused kernel (H never leaves the chip). */
+ *   SMALL: bandwidth-bound D-split kernel (streams B and C once per 32 rows; fp32).
+ *   FUSED: large-batch fused kernel (H never leaves the chip).
+ * AUTO: SMALL for N <= 32 (N <= 8 for TF32 / BF16 models), else FUSED. */
 typedef enum { HDC_PATH_AUTO = 0, HDC_PATH_SMALL = 1, HDC_PATH_FUSED = 2 } hdc_path_t;
 
 typedef struct hdc_model_s* hdc_model_t;

@@ -40,6 +40,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr int64_t kMaxF = int64_t(1) << 20;
 constexpr int kSmallMaxN = 32;
+constexpr int kSmallMaxNLowp = 8;          // bf16 / tf32 models (see run())
 constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 
 }  // namespace
@@ -267,9 +268,10 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
     if (e == cudaSuccess) e = cudaMemset(m->corr, 0, sizeof(long long) * rows * kp);
     if (e == cudaSuccess) e = cudaMalloc((void**)&m->dirty, sizeof(unsigned) * rows);
     if (e == cudaSuccess) e = cudaMemset(m->dirty, 0, sizeof(unsigned) * rows);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_ws, sizeof(float) * rows * m->K);
     m->flag_cap = cap;
   }
+  // scores scratch: int8 mode's provisional scores; every mode's split-N-tile sums
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_ws, sizeof(float) * rows * m->K);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(HDC_ERR_NO_MEMORY, "tensor-core workspace allocation");
@@ -322,8 +324,9 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.dirty = m->dirty;
   o.hout = m->hout;
   o.hout_ldw = m->hout_ldw;
-  // int8 mode: the fused kernel always writes (provisional) scores, corrected afterwards
-  float* S = (mode == 2 && !scores) ? m->S_ws : scores;
+  // the fused kernel always writes scores (int8 mode: provisional, corrected afterwards;
+  // all modes: split N-tiles sum their partials there before the argmax)
+  float* S = scores ? scores : m->S_ws;
   m->tic(st);
   e = launch_fused_tc(mode, o, N, S, labels, m->num_sms, st);
   m->toc(st);
@@ -369,7 +372,14 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
   const ModelView mv = m->view();
   const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC ||
                         !tc_eligible(m));  // FFMA/small kernels are fp32: keep them sign-exact
-  if (path == HDC_PATH_AUTO) path = (N <= kSmallMaxN) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
+  if (path == HDC_PATH_AUTO) {
+    // bf16 / tf32 models: the fused tensor-core kernel beats the fp32 streaming kernel
+    // from N = 16 at cfg3 (tools/smalln_probe.py: N=16 35 vs 40 us, N=32 41 vs 61 us);
+    // fp32 semantics keep the streaming kernel up to 32 rows
+    const int64_t small_max = (tc_eligible(m) && (m->prec == HDC_PREC_BF16 || m->prec == HDC_PREC_TF32))
+                                  ? kSmallMaxNLowp : kSmallMaxN;
+    path = (N <= small_max) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
+  }
   if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
   const SmallWorkspace ws = m->small_ws();
   const int chunk = small_max_rows(m->F, m->D, m->K, m->num_sms);

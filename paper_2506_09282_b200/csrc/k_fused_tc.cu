@@ -857,7 +857,64 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      if (*s_flag && cq == 0 && row_ok) {
+      const int P = (c_last - c_first + 1) * CLD;     // partials per row of this N-tile
+      // slot of this N-tile in a contributing CTA's S_part: clusters after c_first start
+      // inside N-group ng (slot 0); c_first may have started in an earlier one
+      const int ng_first = (int)(range_begin(c_first, p.T, p.G) / p.TdG);
+      const int slot_first = (CLD == 1) ? ((ng_first == ng) ? 0 : 1) : (ng - ng_first);
+      auto part_ptr = [&](int idx, int r, int k) {   // partial idx (cluster-major, then D rank)
+        const int cc = c_first + idx / CLD, j = idx % CLD;
+        const int64_t cta = (int64_t)cc * CLS + rn * CLD + j;
+        return p.S_part + ((cta * p.nslot + (cc == c_first ? slot_first : 0)) * BM + r) * p.K + k;
+      };
+      const int64_t r0 = (int64_t)ni * BM;
+      const int nv = (int)((p.N - r0) < BM ? (p.N - r0) : BM);
+      const int pairs = nv > 0 ? nv * K : 0;          // (row, class) sums of this N-tile
+      if (*s_flag && P > 8) {
+        // Many partials (small N: the N-tile's D-range is spread over many clusters). The
+        // sums go to p.scores (always non-null here), then one thread per row takes the
+        // argmax.  Few pairs: a warp per pair, lane l summing partials l, l + 32, ... in
+        // order, then a fixed butterfly.  Otherwise a thread per pair, 8 partial loads in
+        // flight, summed in partial order.  Both deterministic for a given configuration.
+        __threadfence();
+        if (pairs <= 4 * NUM_EPI) {
+          for (int pi = ew; pi < pairs; pi += NUM_EPI) {
+            const int r = pi / K, k = pi - r * K;
+            float sum = 0.f;
+            for (int idx = lane; idx < P; idx += 32) sum += ld_cg(part_ptr(idx, r, k));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0) p.scores[(r0 + r) * p.K + k] = sum;
+          }
+        } else {
+          for (int pi = ew * 32 + lane; pi < pairs; pi += NUM_EPI * 32) {
+            const int r = pi / K, k = pi - r * K;
+            float sum = 0.f;
+            for (int i0 = 0; i0 < P; i0 += 8) {
+              float v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = (i0 + u < P) ? ld_cg(part_ptr(i0 + u, r, k)) : 0.f;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (i0 + u < P) sum = (i0 + u == 0) ? v[u] : sum + v[u];
+            }
+            p.scores[(r0 + r) * p.K + k] = sum;
+          }
+        }
+        named_bar(1, NUM_EPI * 32);
+        if (cq == 0 && row_ok) {
+          int best = 0;
+          float bv = 0.f;
+          for (int k = 0; k < K; ++k) {
+            const float v = p.scores[row * p.K + k];
+            if (k == 0 || v > bv) {
+              bv = v;
+              best = k;
+            }
+          }
+          if (p.labels) p.labels[row] = best;
+        }
+      } else if (*s_flag && cq == 0 && row_ok) {
         __threadfence();
         // KC classes at a time, their partial loads independent (in flight together);
         // per class the sum order is fixed: cluster, then D rank (bit-deterministic)
@@ -866,20 +923,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         float bv = 0.f;
         for (int k0 = 0; k0 < K; k0 += KC) {
           float acc[KC];
-          bool first = true;
-          for (int cc = c_first; cc <= c_last; ++cc) {
-            const int ng0 = (int)(range_begin(cc, p.T, p.G) / p.TdG);
-            const int slot = (CLD == 1) ? ((ng0 == ng) ? 0 : 1) : (ng - ng0);
-            for (int j = 0; j < CLD; ++j) {
-              const int64_t cta = (int64_t)cc * CLS + rn * CLD + j;
-              const float* src = p.S_part + ((cta * p.nslot + slot) * BM + m) * p.K + k0;
-              float v[KC];
+          for (int idx = 0; idx < P; ++idx) {
+            const float* src = part_ptr(idx, m, k0);
+            float v[KC];
 #pragma unroll
-              for (int u = 0; u < KC; ++u) v[u] = (k0 + u < K) ? ld_cg(src + u) : 0.f;
+            for (int u = 0; u < KC; ++u) v[u] = (k0 + u < K) ? ld_cg(src + u) : 0.f;
 #pragma unroll
-              for (int u = 0; u < KC; ++u) acc[u] = first ? v[u] : acc[u] + v[u];
-              first = false;
-            }
+            for (int u = 0; u < KC; ++u) acc[u] = idx == 0 ? v[u] : acc[u] + v[u];
           }
 #pragma unroll
           for (int u = 0; u < KC; ++u) {

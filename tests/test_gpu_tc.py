@@ -112,3 +112,22 @@ def test_tc_cta_pair_mode(hdc, monkeypatch, prec, N, F, D, K):
     print(prec, (N, F, D, K), rep)
     assert np.array_equal(out["2x1"][0], out["2x1p"][0])
     np.testing.assert_allclose(out["2x1"][1], out["2x1p"][1], rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("prec", ["fp32_tc", "bf16"])
+@pytest.mark.parametrize("N", [1, 5, 32, 200])
+def test_tc_small_batch_fused(hdc, prec, N):
+    # small N on the fused kernel: one N-tile's D-range spread over up to 148 CTAs, so the
+    # last arriver sums many partials (warp-cooperative reduction, fixed order)
+    cfg = CONFIGS["cfg3_n32"]
+    X = make_X(cfg, 0, N)                                       # rows of the cfg3 X stream
+    B, C = make_B(cfg), make_C(cfg)
+    Bd, Cd = to_dev(B, C)
+    m = hdc.Model(Bd, Cd, prec=prec)
+    y, S = run_model(m, X, "fused")
+    y2, S2 = run_model(m, X, "fused")
+    m.close()
+    assert np.array_equal(y, y2) and np.array_equal(S, S2)          # deterministic
+    orc = oracle.infer(X, B, C, allow=True)
+    rep = check_fp32(orc, y, S) if prec == "fp32_tc" else check_lowp(orc, y, S)
+    print(prec, N, rep)
