@@ -985,7 +985,11 @@ __device__ __forceinline__ float scale_for(float amax) {
 }
 
 // One warp per row of a row-major [rows][F] fp32 matrix (X rows, or B^T rows):
-// int8 limbs into out[l][rows_p][Fp] and the per-row tau term.
+// int8 limbs into out[l][rows_p][Fp] and the per-row tau term.  Lane `lane` owns the
+// groups of four consecutive elements f0 = 4 lane + 128 i (one 4-byte store per limb;
+// Fp is a multiple of 64, so a group is entirely inside or outside [0, Fp)).  With
+// NG > 0 the row is read once into registers (Fp <= 128 NG); NG = 0 reads it twice.
+template <int NG>
 __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
                                  int64_t F, int64_t ld_src, int64_t Fp, int8_t* __restrict__ out,
                                  int64_t* __restrict__ tau_part, int64_t tau_const) {
@@ -993,21 +997,54 @@ __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, in
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (r >= rows_p) return;
   const bool valid = r < rows;
+  const float* __restrict__ row = src + r * ld_src;
+  float xs[NG > 0 ? 4 * NG : 1];
   float amax = 0.f;
-  if (valid)
-    for (int64_t f = lane; f < F; f += 32) amax = fmaxf(amax, fabsf(src[r * ld_src + f]));
+  if constexpr (NG > 0) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t f = 4 * lane + 128 * g + e;
+        xs[4 * g + e] = (valid && f < F) ? __ldg(row + f) : 0.f;
+        amax = fmaxf(amax, fabsf(xs[4 * g + e]));
+      }
+  } else if (valid) {
+#pragma unroll 4
+    for (int64_t f = lane; f < F; f += 32) amax = fmaxf(amax, fabsf(row[f]));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   const float c = scale_for(amax);
   long long l1 = 0;
-  for (int64_t f = lane; f < Fp; f += 32) {
-    const float x = (valid && f < F) ? src[r * ld_src + f] : 0.f;
-    int d0, d1, d2, U;
-    limbs_of(x, c, d0, d1, d2, U);
-    out[(0 * rows_p + r) * Fp + f] = (int8_t)d0;
-    out[(1 * rows_p + r) * Fp + f] = (int8_t)d1;
-    out[(2 * rows_p + r) * Fp + f] = (int8_t)d2;
-    l1 += U < 0 ? -U : U;
+  auto emit = [&](int64_t f0, const float* x4) {
+    uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int d0, d1, d2, U;
+      limbs_of(x4[e], c, d0, d1, d2, U);
+      w0 |= (uint32_t)(uint8_t)(int8_t)d0 << (8 * e);
+      w1 |= (uint32_t)(uint8_t)(int8_t)d1 << (8 * e);
+      w2 |= (uint32_t)(uint8_t)(int8_t)d2 << (8 * e);
+      l1 += U < 0 ? -U : U;
+    }
+    *reinterpret_cast<uint32_t*>(out + (0 * rows_p + r) * Fp + f0) = w0;
+    *reinterpret_cast<uint32_t*>(out + (1 * rows_p + r) * Fp + f0) = w1;
+    *reinterpret_cast<uint32_t*>(out + (2 * rows_p + r) * Fp + f0) = w2;
+  };
+  if constexpr (NG > 0) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int64_t f0 = 4 * lane + 128 * g;
+      if (f0 < Fp) emit(f0, xs + 4 * g);
+    }
+  } else {
+    for (int64_t f0 = 4 * lane; f0 < Fp; f0 += 128) {
+      float x4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x4[e] = (valid && f0 + e < F) ? row[f0 + e] : 0.f;
+      emit(f0, x4);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
@@ -1311,8 +1348,13 @@ cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int6
                             int64_t Fp, int8_t* out, int64_t* tau_part, int64_t tau_const,
                             cudaStream_t st) {
   const int warps = 8;
-  limb_rows_kernel<<<(unsigned)((rows_p + warps - 1) / warps), warps * 32, 0, st>>>(
-      src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+  const unsigned grid = (unsigned)((rows_p + warps - 1) / warps);
+  if (Fp <= 512)
+    limb_rows_kernel<4><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+  else if (Fp <= 1024)
+    limb_rows_kernel<8><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+  else
+    limb_rows_kernel<0><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
   return cudaGetLastError();
 }
 
