@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--dshard", action="store_true",
                     help="D-shard (small-N): each rank holds a column slice; all-reduce of N x K "
                          "partial scores inside the timed step (strong scaling)")
+    ap.add_argument("--dshard-exchange", default="kernel", choices=["kernel", "nccl"],
+                    help="D-shard reduction: 'kernel' = the small-batch kernel stores its partial "
+                         "into every rank's symmetric-memory buffer and sums them in rank order "
+                         "(hdc_model_infer_dshard, N <= 32); 'nccl' = all-reduce + argmax kernel")
     return ap.parse_args()
 
 
@@ -268,6 +272,14 @@ def run_ours(args, rank, world, local_rank):
     Hbuf = torch.empty(cfg.N, (cfg.D + 31) // 32, dtype=torch.int32, device=dev)
     ytrain = (torch.arange(cfg.N, device=dev, dtype=torch.int32) * 7919) % cfg.K
     counts = torch.zeros(cfg.K, cfg.D, dtype=torch.int32, device=dev)
+    xchg = None
+    if args.dshard and args.dshard_exchange == "kernel" and cfg.N <= 32:
+        from paper_2506_09282_b200.sharding import DShardExchange
+        if not dist.is_initialized():            # the exchange rendezvous needs a process group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        xchg = DShardExchange(cfg.N, cfg.K)
 
     def step():
         if args.mode == "unfused":
@@ -277,6 +289,8 @@ def run_ours(args, rank, world, local_rank):
             model.encode(X, H=Hbuf)
             counts.zero_()
             hdc.bundle_classes(Hbuf, cfg.D, ytrain, cfg.K, counts=counts, return_M=False)
+        elif xchg is not None:
+            xchg.infer(model, X)
         elif args.dshard:
             model.partial_scores(X, out=Sbuf)
             if world > 1:
@@ -290,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches_per_step = model.last_launch_count() + (1 if args.dshard else 0) + \
+    launches_per_step = model.last_launch_count() + (1 if args.dshard and xchg is None else 0) + \
         {"infer": 0, "unfused": 2, "train": 4}[args.mode]   # + memset/similarity, memset/sort/bundle
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -376,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
            "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
                       "prec": args.prec, "path": args.path, "mode": args.mode, "global_batch": units,
                       "parallelism": ("dshard%d" % world) if args.dshard else ("dp%d" % world),
+                      "dshard_exchange": (("kernel" if xchg is not None else "nccl") if args.dshard else None),
                       "l2": "flushed between steps (write of 2x L2 bytes, untimed)",
                       "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

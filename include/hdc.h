@@ -132,6 +132,25 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
 hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, float* S_partial,
                                       void* stream);
 
+/* D-shard inference with the reduction inside the kernel (Alg. 3 `S += S_local`, P:336,
+ * across GPUs; SURVEY §8 f2 over peer memory): every rank calls this with its D-slice
+ * model, the same X (N rows, 1 <= N <= 32), the same `epoch` (a call counter that
+ * increases by one per call, identical on all ranks) and `xbufs`, a DEVICE array of
+ * `world` pointers: the exchange buffer of each rank, mapped into this process (CUDA IPC
+ * / symmetric memory; xbufs[rank] is this rank's own).  Each buffer holds
+ * hdc_dshard_exchange_bytes(N, K, world) bytes (world uint32 signal words, padded to 16
+ * bytes, then 2 x world slots of N*K floats) and must be zeroed once before the first
+ * call (epoch 1 is the first valid epoch; the buffer may serve any N up to its size).  The small-batch kernel's last CTA stores this
+ * rank's partial scores into every rank's buffer (peer stores), release-signals them,
+ * waits until all ranks' partials arrived and sums them in rank order, so labels and
+ * scores (N*K, optional) are identical on every rank.  One launch, no NCCL.  The ranks'
+ * kernels wait on one another: launch them on different GPUs only.
+ * Errors: UNSUPPORTED (N > 32, shapes outside the streaming kernel), INVALID_VALUE. */
+int64_t hdc_dshard_exchange_bytes(int64_t N, int64_t K, int world);
+hdc_status_t hdc_model_infer_dshard(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                                    float* scores, float* const* xbufs, int rank, int world,
+                                    uint32_t epoch, void* stream);
+
 /* Row argmax, lowest index among equal maxima: labels[n] = argmax_k S[n*K+k]. */
 hdc_status_t hdc_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, void* stream);
 

@@ -555,6 +555,38 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
   return run(m, X, N, nullptr, S_partial, HDC_PATH_AUTO, (cudaStream_t)stream);
 }
 
+int64_t hdc_dshard_exchange_bytes(int64_t N, int64_t K, int world) {
+  if (N < 1 || K < 1 || world < 1) return 0;
+  const int64_t stride = (N * K + 3) / 4 * 4, sigpad = (world + 3) / 4 * 4;
+  return (int64_t)4 * (sigpad + 2 * world * stride);
+}
+
+hdc_status_t hdc_model_infer_dshard(hdc_model_t m, const float* X, int64_t N, int32_t* labels,
+                                    float* scores, float* const* xbufs, int rank, int world,
+                                    uint32_t epoch, void* stream) {
+  hdc_status_t st = validate_call(m, X, N, labels, scores);
+  if (st != HDC_OK) return st;
+  if (N < 1 || N > kSmallMaxN) return fail(HDC_ERR_UNSUPPORTED, "D-shard exchange: 1 <= N <= 32");
+  if (world < 1 || rank < 0 || rank >= world) return fail(HDC_ERR_INVALID_VALUE, "rank / world");
+  if (!xbufs || !aligned(xbufs, 8)) return fail(HDC_ERR_INVALID_VALUE, "null or misaligned xbufs");
+  if (!m->B4 || !smallstream_fits(m->F, m->D, m->K, (int)N, m->num_sms) ||
+      small_max_rows(m->F, m->D, m->K, m->num_sms) < N)
+    return fail(HDC_ERR_UNSUPPORTED, "shapes outside the small-batch streaming kernel");
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
+  cudaStream_t s = (cudaStream_t)stream;
+  const DshardExchange xc{xbufs, rank, world, epoch};
+  const bool recheck = true;                   // the streaming kernel is fp32: keep it sign-exact
+  m->last_launches = 0;
+  m->tic(s);
+  cudaError_t e = launch_smallstream(m->view(), m->small_ws(), X, (int)N, scores, labels, recheck,
+                                     m->num_sms, s, &xc);
+  m->toc(s);
+  if (e != cudaSuccess) return cuda_fail(e, "D-shard small-batch launch");
+  m->last_launches = 1;
+  return HDC_OK;
+}
+
 hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                                   int32_t* labels_host, float* scores_host, void* stream) {
   hdc_status_t st = validate_call(m, X_host, N, labels_host, scores_host);

@@ -58,6 +58,11 @@ struct StreamParams {
   float* scores;
   int32_t* labels;
   unsigned long long* dbg;   // diagnostics (HDC_SMALL_DEBUG): [0] min start, [1..7] max of phase ends (ns)
+  // D-shard exchange (hdc_model_infer_dshard): xworld > 0 -> the last CTA sends this
+  // rank's partial scores to every rank's exchange buffer and sums all ranks' partials
+  float* const* xbufs;       // [xworld] device pointers (peer-mapped) of the exchange buffers
+  int xrank, xworld;
+  uint32_t xepoch;           // call number, identical on all ranks, increasing
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -378,6 +383,44 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
     cbar();
   }
   SS_MARK(4);
+  if (p.xworld > 0) {
+    // ---- D-shard exchange over peer memory (Alg. 3 `S += S_local`, across GPUs):
+    // buffer of rank r = xworld uint32 signals (padded to 4 words), then
+    // [2 parities][xworld senders][xstride] floats.  (1) store this rank's S_local into slot (parity, xrank) of every
+    // rank's buffer (peer stores over NVLink), (2) fence, release-store the epoch into
+    // signal[xrank] of every rank, (3) acquire-wait until all signals of our own buffer
+    // reached the epoch, (4) sum the slots in rank order: identical on every rank.
+    // Parity double-buffering: a rank writes slot parity e & 1 of call e only after it
+    // received every rank's call e-1 signal, i.e. after they finished reading call e-2.
+    const int W = p.xworld, par = (int)(p.xepoch & 1u);
+    const int xstride = (nk + 3) & ~3, sigpad = (W + 3) & ~3;
+    for (int r = 0; r < W; ++r) {
+      float* dst = p.xbufs[r] + sigpad + ((size_t)par * W + p.xrank) * xstride;
+      for (int i = tid; i < nk; i += kCt) dst[i] = Sfin[i];
+    }
+    __threadfence_system();
+    cbar();
+    if (tid < W) {
+      uint32_t* sig = reinterpret_cast<uint32_t*>(p.xbufs[tid]);
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig + p.xrank), "r"(p.xepoch) : "memory");
+    }
+    if (tid < W) {
+      const uint32_t* sig = reinterpret_cast<const uint32_t*>(p.xbufs[p.xrank]);
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sig + tid) : "memory");
+      } while ((int32_t)(v - p.xepoch) < 0);
+    }
+    cbar();
+    const float* own = p.xbufs[p.xrank] + sigpad + (size_t)par * W * xstride;
+    for (int i = tid; i < nk; i += kCt) {
+      float a = own[i];
+      for (int r = 1; r < W; ++r) a += own[(size_t)r * xstride + i];
+      Sfin[i] = a;
+      if (p.scores) p.scores[i] = a;
+    }
+    cbar();
+  }
   if (p.labels)
     for (int n = tid; n < p.nrows; n += kCt) {
       int best = 0;
@@ -444,8 +487,12 @@ bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms) {
 
 cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, const float* X, int n,
                                float* scores, int32_t* labels, bool recheck, int num_sms,
-                               cudaStream_t st) {
+                               cudaStream_t st, const DshardExchange* xc) {
   StreamParams p;
+  p.xbufs = xc ? xc->bufs : nullptr;
+  p.xrank = xc ? xc->rank : 0;
+  p.xworld = xc ? xc->world : 0;
+  p.xepoch = xc ? xc->epoch : 0u;
   p.X = X;
   p.nrows = n;
   p.F = m.F;

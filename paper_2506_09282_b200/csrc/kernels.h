@@ -40,9 +40,15 @@ cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, cons
 
 // K2s (k_smallstream.cu): TMA-streamed small-batch kernel, rows [0, n), n <= 32.
 bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms);
+// In-kernel D-shard exchange of the small-batch kernel (hdc_model_infer_dshard).
+struct DshardExchange {
+  float* const* bufs;   // device array [world] of the ranks' exchange buffers
+  int rank, world;
+  uint32_t epoch;
+};
 cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, const float* X, int n,
                                float* scores, int32_t* labels, bool recheck, int num_sms,
-                               cudaStream_t st);
+                               cudaStream_t st, const DshardExchange* xc = nullptr);
 
 // Workspace of the fused large-batch kernels (grown with N).
 struct FusedWorkspace {

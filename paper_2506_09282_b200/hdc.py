@@ -41,6 +41,9 @@ def lib():
         L.hdc_model_infer_host.argtypes = [P, P, I64, P, P, P]
         L.hdc_model_partial_scores.argtypes = [P, P, I64, P, P]
         L.hdc_argmax.argtypes = [P, I64, I64, P, P]
+        L.hdc_model_infer_dshard.argtypes = [P, P, I64, P, P, P, I32, I32, ctypes.c_uint32, P]
+        L.hdc_dshard_exchange_bytes.argtypes = [I64, I64, I32]
+        L.hdc_dshard_exchange_bytes.restype = I64
         L.hdc_model_encode.argtypes = [P, P, I64, P, I64, P]
         L.hdc_similarity_packed.argtypes = [P, I64, I64, I64, P, I64, P, P, P]
         L.hdc_bundle_classes.argtypes = [P, I64, I64, I64, P, I64, P, P, P]
@@ -60,6 +63,7 @@ def lib():
         L.hdc_version.restype = ctypes.c_char_p
         for name in ("hdc_infer", "hdc_model_create", "hdc_model_infer", "hdc_model_infer_path",
                      "hdc_model_infer_host", "hdc_model_partial_scores", "hdc_argmax",
+                     "hdc_model_infer_dshard",
                      "hdc_model_destroy", "hdc_model_dims", "hdc_model_encode",
                      "hdc_similarity_packed", "hdc_bundle_classes"):
             getattr(L, name).restype = I32
@@ -157,6 +161,26 @@ class Model:
                                                   _stream_ptr(stream, X.device)))
         return out
 
+    def infer_dshard(self, X, xbufs, rank, world, epoch, labels=None, scores=None, return_scores=False,
+                     stream=None):
+        """D-shard inference with the cross-rank sum inside the kernel
+        (hdc_model_infer_dshard): `xbufs` is a CUDA int64 tensor of the `world` exchange
+        buffer addresses (this rank's D-slice model; same X, N <= 32 and epoch on all ranks)."""
+        X = _dev_f32(X, "X")
+        if not (isinstance(xbufs, torch.Tensor) and xbufs.is_cuda and xbufs.dtype == torch.int64
+                and xbufs.numel() == world):
+            raise TypeError("xbufs must be a CUDA int64 tensor of `world` addresses")
+        N = X.shape[0]
+        if labels is None:
+            labels = torch.empty(N, dtype=torch.int32, device=X.device)
+        if scores is None and return_scores:
+            scores = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        with torch.cuda.device(self.device):
+            _check(lib().hdc_model_infer_dshard(self._h, _ptr(X), N, _ptr(labels), _ptr(scores), _ptr(xbufs),
+                                                int(rank), int(world), int(epoch) & 0xFFFFFFFF,
+                                                _stream_ptr(stream, X.device)))
+        return labels, scores
+
     def recheck_count(self):
         return int(lib().hdc_model_recheck_count(self._h))
 
@@ -193,6 +217,11 @@ def infer(X, B, C, prec="fp32", return_scores=False, stream=None):
         _check(lib().hdc_infer(_ptr(X), _ptr(B), _ptr(C), N, F, D, K, _ptr(labels), _ptr(scores),
                                PREC[prec], _stream_ptr(stream, X.device)))
     return labels, scores
+
+
+def dshard_exchange_bytes(N, K, world):
+    """Bytes of one rank's exchange buffer for hdc_model_infer_dshard."""
+    return int(lib().hdc_dshard_exchange_bytes(int(N), int(K), int(world)))
 
 
 def argmax(S, labels=None, stream=None):

@@ -13,6 +13,12 @@ Two partitions, following the paper's two Stage II variants:
   (hdc_model_partial_scores), the ranks sum them with one all-reduce of N x K
   fp32 (Alg. 3 `S += S_local`) and take the lowest-index argmax.
 
+* D-shard with the reduction in the kernel (``DShardExchange``, SURVEY §8 f2 over peer
+  memory): the small-batch kernel's last CTA stores S_r into every rank's exchange
+  buffer (torch symmetric memory, peer-mapped), signals, waits for all ranks and sums
+  the partials in rank order -- one launch, no NCCL call, identical results on all
+  ranks.
+
 torch.distributed (NCCL on GPUs) is plumbing only.  The per-rank compute is
 delegated to an object with the ``Model`` interface (``infer`` /
 ``partial_scores``), normally ``paper_2506_09282_b200.Model``.
@@ -70,3 +76,38 @@ def shard_d_infer(model_slice, X, argmax_fn, return_scores=False, group=None):
     dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
     labels = argmax_fn(S)
     return labels, (S if return_scores else None)
+
+
+class DShardExchange:
+    """Exchange buffers for the in-kernel D-shard reduction (hdc_model_infer_dshard).
+
+    Allocated with torch symmetric memory (``torch.distributed._symmetric_memory``), so
+    every rank's buffer is mapped into every process; the device array of the `world`
+    buffer addresses is what the kernel writes through.  ``n_max`` bounds the batch
+    rows (<= 32), ``K`` is the class count.  Collective: all ranks construct it together
+    and then call :meth:`infer` the same number of times with the same X shape."""
+
+    def __init__(self, n_max, K, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm
+        from .hdc import dshard_exchange_bytes
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = dshard_exchange_bytes(n_max, K, self.world)
+        self.n_max = n_max
+        self.buf = symm.empty(nbytes // 4, dtype=torch.float32, device=dev)
+        self.buf.zero_()
+        handle = symm.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.ptrs = torch.tensor([int(p) for p in handle.buffer_ptrs], dtype=torch.int64, device=dev)
+        self.epoch = 0
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    def infer(self, model_slice, X, return_scores=False, stream=None):
+        """Labels (and scores) of X on every rank; `model_slice` holds this rank's D-slice."""
+        if X.shape[0] > self.n_max:
+            raise ValueError("X has %d rows, the exchange was sized for %d" % (X.shape[0], self.n_max))
+        self.epoch += 1
+        return model_slice.infer_dshard(X, self.ptrs, self.rank, self.world, self.epoch,
+                                        return_scores=return_scores, stream=stream)

@@ -43,3 +43,66 @@ def test_nshard_and_dshard_world1(nccl_group):
     torch.cuda.synchronize()
     assert torch.equal(y2, y3) and torch.equal(S2, S3)
     m.close()
+
+
+def test_dshard_in_kernel_exchange_world1(nccl_group):
+    # the in-kernel D-shard reduction over torch symmetric memory, one rank: the exchange
+    # runs (store, signal, wait, sum of one slot) and equals the plain small-batch call
+    import paper_2506_09282_b200 as hdc
+    from paper_2506_09282_b200.sharding import DShardExchange
+    cfg = CONFIGS["cfg3_n32"]
+    X, B, C = make_X(cfg), make_B(cfg), make_C(cfg)
+    Xd, Bd, Cd = to_dev(X, B, C)
+    m = hdc.Model(Bd, Cd, prec="fp32")
+    xc = DShardExchange(32, cfg.K)
+    for n in (1, 7, 32, 32, 3):                      # several epochs, both parities
+        y, S = xc.infer(m, Xd[:n], return_scores=True)
+        y0, S0 = m.infer(Xd[:n], path="small", return_scores=True)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0) and torch.equal(S, S0)
+    m.close()
+
+
+def _slot(buf, world, stride, parity, sender):
+    sigpad = (world + 3) // 4 * 4
+    off = sigpad + (parity * world + sender) * stride
+    return buf[off:off + stride]
+
+
+@pytest.mark.parametrize("N", [1, 13, 32])
+def test_dshard_exchange_two_ranks_simulated(cuda_device, N):
+    # Rank 0 of a 2-rank exchange on one GPU, WITHOUT a second kernel: rank 1's partial and
+    # its signal are placed in rank 0's buffer beforehand, so the kernel never waits on
+    # another kernel.  Checks the rank-order sum, the stores into the peer buffer and the
+    # signals, for both parities.
+    import paper_2506_09282_b200 as hdc
+    cfg = CONFIGS["cfg3_n32"]
+    X, B, C = make_X(cfg, 0, N), make_B(cfg), make_C(cfg)
+    Xd, Bd, Cd = to_dev(X, B, C)
+    cut = 4996                                        # multiple of 4 (d_shard_slices alignment)
+    ma = hdc.Model(Bd[:, :cut].contiguous(), Cd[:, :cut].contiguous(), prec="fp32")
+    mb = hdc.Model(Bd[:, cut:].contiguous(), Cd[:, cut:].contiguous(), prec="fp32")
+    W, K = 2, cfg.K
+    nwords = hdc.dshard_exchange_bytes(N, K, W) // 4
+    stride = (N * K + 3) // 4 * 4
+    bufs = [torch.zeros(nwords, dtype=torch.float32, device="cuda") for _ in range(W)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    Sa = ma.partial_scores(Xd)
+    Sb = mb.partial_scores(Xd)
+    for epoch in (1, 2, 3):
+        par = epoch & 1
+        _slot(bufs[0], W, stride, par, 1)[:N * K] = Sb.reshape(-1)            # rank 1's partial
+        bufs[0][:W].view(torch.int32)[1] = epoch                              # ... and its signal
+        y, S = ma.infer_dshard(Xd, ptrs, 0, W, epoch, return_scores=True)
+        torch.cuda.synchronize()
+        expect = Sa + Sb                                                      # rank order
+        assert torch.equal(S, expect)
+        assert torch.equal(y, hdc.argmax(expect))
+        assert torch.equal(_slot(bufs[1], W, stride, par, 0)[:N * K], Sa.reshape(-1))   # sent to rank 1
+        assert int(bufs[1][:W].view(torch.int32)[0]) == epoch                 # rank 1 signalled
+        assert int(bufs[0][:W].view(torch.int32)[0]) == epoch
+    # argument checks
+    with pytest.raises(hdc.HDCError):
+        ma.infer_dshard(Xd, ptrs, 2, W, 4)
+    ma.close()
+    mb.close()
