@@ -984,93 +984,186 @@ __device__ __forceinline__ float scale_for(float amax) {
   return (float)c * (1.f - 9.5367431640625e-07f);  // (1 - 2^-20): keeps |x c| < 127*2^14
 }
 
-// One warp per row of a row-major [rows][F] fp32 matrix (X rows, or B^T rows):
-// int8 limbs into out[l][rows_p][Fp] and the per-row tau term.  Lane `lane` owns the
-// groups of four consecutive elements f0 = 4 lane + 128 i (one 4-byte store per limb;
-// Fp is a multiple of 64, so a group is entirely inside or outside [0, Fp)).  With
-// NG > 0 the row is read once into registers (Fp <= 128 NG); NG = 0 reads it twice.
+// Four consecutive elements f0..f0+3 of a source row (zero past F and for padding rows);
+// one 16-byte load when the row start and f0 are 16-byte aligned and all four are < F.
+__device__ __forceinline__ void load4(const float* __restrict__ row, int64_t f0, int64_t F, bool valid,
+                                      bool vec, float* x) {
+  if (valid && vec && f0 + 3 < F) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(row + f0));
+    x[0] = v.x;
+    x[1] = v.y;
+    x[2] = v.z;
+    x[3] = v.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = (valid && f0 + e < F) ? __ldg(row + f0 + e) : 0.f;
+  }
+}
+
+// int8 limbs of four elements -> one 4-byte store per limb; returns their L1(U).
+__device__ __forceinline__ long long emit_limbs4(const float* x, float c, int8_t* __restrict__ out,
+                                                 int64_t rows_p, int64_t r, int64_t Fp, int64_t f0) {
+  uint32_t w0 = 0, w1 = 0, w2 = 0;
+  long long l1 = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int d0, d1, d2, U;
+    limbs_of(x[e], c, d0, d1, d2, U);
+    w0 |= (uint32_t)(uint8_t)(int8_t)d0 << (8 * e);
+    w1 |= (uint32_t)(uint8_t)(int8_t)d1 << (8 * e);
+    w2 |= (uint32_t)(uint8_t)(int8_t)d2 << (8 * e);
+    l1 += U < 0 ? -U : U;
+  }
+  *reinterpret_cast<uint32_t*>(out + (0 * rows_p + r) * Fp + f0) = w0;
+  *reinterpret_cast<uint32_t*>(out + (1 * rows_p + r) * Fp + f0) = w1;
+  *reinterpret_cast<uint32_t*>(out + (2 * rows_p + r) * Fp + f0) = w2;
+  return l1;
+}
+
+// tau of a row from its L1(U): |c_x c_b x.b - U_x.U_b| <= 0.625 (L1(U_x) + L1(U_b)) +
+// 0.3907 F and the dropped limb products (i + j >= 3) add <= F (2^20 + 2^12) (DESIGN.md
+// §4).  The kernel compares I = A0 2^14 + A1 2^7 + A2 = (U_x.U_b - dropped) / 2^14, so
+// tau is stored / 2^14, rounded up: ceil((5 l1 / 8 + tau_const) / 2^14)
+// = (5 l1 + 8 tau_const + 2^17 - 1) >> 17.
+__device__ __forceinline__ int64_t row_tau(long long l1, int64_t tau_const, bool valid) {
+  return valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : -(int64_t(1) << 62);
+}
+
+// One warp per row of a row-major [rows][F] fp32 matrix (X rows, or B^T rows): int8
+// limbs into out[l][rows_p][Fp] and the per-row tau term.  Lane `lane` owns the groups
+// of four elements f0 = 4 lane + 128 g (Fp is a multiple of 64, so a group is entirely
+// inside or outside [0, Fp)); the row is read once into registers (Fp <= 128 NG).
 template <int NG>
 __global__ void limb_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
                                  int64_t F, int64_t ld_src, int64_t Fp, int8_t* __restrict__ out,
-                                 int64_t* __restrict__ tau_part, int64_t tau_const) {
+                                 int64_t* __restrict__ tau_part, int64_t tau_const, bool vec) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (r >= rows_p) return;
   const bool valid = r < rows;
   const float* __restrict__ row = src + r * ld_src;
-  float xs[NG > 0 ? 4 * NG : 1];
+  float xs[4 * NG];
   float amax = 0.f;
-  if constexpr (NG > 0) {
 #pragma unroll
-    for (int g = 0; g < NG; ++g)
+  for (int g = 0; g < NG; ++g) {
+    load4(row, 4 * lane + 128 * g, F, valid, vec, xs + 4 * g);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int64_t f = 4 * lane + 128 * g + e;
-        xs[4 * g + e] = (valid && f < F) ? __ldg(row + f) : 0.f;
-        amax = fmaxf(amax, fabsf(xs[4 * g + e]));
-      }
-  } else if (valid) {
-#pragma unroll 4
-    for (int64_t f = lane; f < F; f += 32) amax = fmaxf(amax, fabsf(row[f]));
+    for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(xs[4 * g + e]));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   const float c = scale_for(amax);
   long long l1 = 0;
-  auto emit = [&](int64_t f0, const float* x4) {
-    uint32_t w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      int d0, d1, d2, U;
-      limbs_of(x4[e], c, d0, d1, d2, U);
-      w0 |= (uint32_t)(uint8_t)(int8_t)d0 << (8 * e);
-      w1 |= (uint32_t)(uint8_t)(int8_t)d1 << (8 * e);
-      w2 |= (uint32_t)(uint8_t)(int8_t)d2 << (8 * e);
-      l1 += U < 0 ? -U : U;
-    }
-    *reinterpret_cast<uint32_t*>(out + (0 * rows_p + r) * Fp + f0) = w0;
-    *reinterpret_cast<uint32_t*>(out + (1 * rows_p + r) * Fp + f0) = w1;
-    *reinterpret_cast<uint32_t*>(out + (2 * rows_p + r) * Fp + f0) = w2;
-  };
-  if constexpr (NG > 0) {
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int64_t f0 = 4 * lane + 128 * g;
-      if (f0 < Fp) emit(f0, xs + 4 * g);
-    }
-  } else {
-    for (int64_t f0 = 4 * lane; f0 < Fp; f0 += 128) {
-      float x4[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) x4[e] = (valid && f0 + e < F) ? row[f0 + e] : 0.f;
-      emit(f0, x4);
-    }
+  for (int g = 0; g < NG; ++g) {
+    const int64_t f0 = 4 * lane + 128 * g;
+    if (f0 < Fp) l1 += emit_limbs4(xs + 4 * g, c, out, rows_p, r, Fp, f0);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-  // |c_x c_b x.b - U_x.U_b| <= 0.625 (L1(U_x) + L1(U_b)) + 0.3907 F and the dropped limb
-  // products (i + j >= 3) add <= F (2^20 + 2^12).  The kernel compares
-  // I = A0 2^14 + A1 2^7 + A2 = (U_x.U_b - dropped) / 2^14, so tau is stored / 2^14,
-  // rounded up: ceil((5 l1 / 8 + tau_const) / 2^14) = (5 l1 + 8 tau_const + 2^17 - 1) >> 17.
-  if (lane == 0 && tau_part)
-    tau_part[r] = valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : -(int64_t(1) << 62);
+  if (lane == 0 && tau_part) tau_part[r] = row_tau(l1, tau_const, valid);
 }
 
-// Rounded copies for the bf16 / tf32 modes: out[r][f] (rows_p x Fp, zero padded).
+// Long rows (Fp > 1024): one 256-thread block per row, thread t owning the groups
+// f0 = 4 t + 1024 g (Fp <= 1024 NGB); block reductions for max |x| and L1(U).
+template <int NGB>
+__global__ void __launch_bounds__(256) limb_rows_block_kernel(const float* __restrict__ src, int64_t rows,
+                                                              int64_t rows_p, int64_t F, int64_t ld_src,
+                                                              int64_t Fp, int8_t* __restrict__ out,
+                                                              int64_t* __restrict__ tau_part,
+                                                              int64_t tau_const, bool vec) {
+  __shared__ float s_max[8];
+  __shared__ long long s_l1[8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t r = blockIdx.x;
+  const bool valid = r < rows;
+  const float* __restrict__ row = src + r * ld_src;
+  float xs[4 * NGB];
+  float amax = 0.f;
+#pragma unroll
+  for (int g = 0; g < NGB; ++g) {
+    load4(row, 4 * t + 1024 * g, F, valid, vec, xs + 4 * g);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(xs[4 * g + e]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) s_max[w] = amax;
+  __syncthreads();
+  amax = s_max[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) amax = fmaxf(amax, s_max[i]);
+  const float c = scale_for(amax);
+  long long l1 = 0;
+#pragma unroll
+  for (int g = 0; g < NGB; ++g) {
+    const int64_t f0 = 4 * t + 1024 * g;
+    if (f0 < Fp) l1 += emit_limbs4(xs + 4 * g, c, out, rows_p, r, Fp, f0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  if (lane == 0) s_l1[w] = l1;
+  __syncthreads();
+  if (t == 0 && tau_part) {
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += s_l1[i];
+    tau_part[r] = row_tau(s, tau_const, valid);
+  }
+}
+
+// Two-pass fallback for very long rows (Fp > 4096): one warp per row.
+__global__ void limb_rows_2pass_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p, int64_t F,
+                                       int64_t ld_src, int64_t Fp, int8_t* __restrict__ out,
+                                       int64_t* __restrict__ tau_part, int64_t tau_const, bool vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows_p) return;
+  const bool valid = r < rows;
+  const float* __restrict__ row = src + r * ld_src;
+  float amax = 0.f;
+  for (int64_t f0 = 4 * lane; f0 < Fp; f0 += 128) {
+    float x[4];
+    load4(row, f0, F, valid, vec, x);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(x[e]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float c = scale_for(amax);
+  long long l1 = 0;
+  for (int64_t f0 = 4 * lane; f0 < Fp; f0 += 128) {
+    float x[4];
+    load4(row, f0, F, valid, vec, x);
+    l1 += emit_limbs4(x, c, out, rows_p, r, Fp, f0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  if (lane == 0 && tau_part) tau_part[r] = row_tau(l1, tau_const, valid);
+}
+
+// Rounded copies for the bf16 / tf32 modes: out[r][f] (rows_p x Fp, zero padded), four
+// elements per thread (16-byte loads when aligned, 8 / 16-byte stores).
 template <int MODE>
 __global__ void round_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t rows_p,
-                                  int64_t F, int64_t ld_src, int64_t Fp, void* __restrict__ out) {
-  const int64_t total = rows_p * Fp;
+                                  int64_t F, int64_t ld_src, int64_t Fp, void* __restrict__ out, bool vec) {
+  const int64_t gpr = Fp / 4, total = rows_p * gpr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / Fp, f = i % Fp;
-    const float x = (r < rows && f < F) ? src[r * ld_src + f] : 0.f;
+    const int64_t r = i / gpr, f0 = 4 * (i - r * gpr);
+    float x[4];
+    load4(src + r * ld_src, f0, F, r < rows, vec, x);
     if constexpr (MODE == 0) {
-      reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(x);
+      __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]), b = __floats2bfloat162_rn(x[2], x[3]);
+      uint2 v;
+      v.x = *reinterpret_cast<uint32_t*>(&a);
+      v.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + r * Fp + f0) = v;
     } else {
-      uint32_t y;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
-      reinterpret_cast<uint32_t*>(out)[i] = y;
+      uint32_t y[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y[e]) : "f"(x[e]));
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(out) + r * Fp + f0) = make_uint4(y[0], y[1], y[2], y[3]);
     }
   }
 }
@@ -1347,14 +1440,23 @@ int64_t tc_tau_const(int64_t F) {
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
                             int64_t Fp, int8_t* out, int64_t* tau_part, int64_t tau_const,
                             cudaStream_t st) {
+  // 16-byte loads need 16-byte aligned rows
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (ld_src % 4 == 0);
   const int warps = 8;
   const unsigned grid = (unsigned)((rows_p + warps - 1) / warps);
   if (Fp <= 512)
-    limb_rows_kernel<4><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+    limb_rows_kernel<4><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const, vec);
   else if (Fp <= 1024)
-    limb_rows_kernel<8><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+    limb_rows_kernel<8><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const, vec);
+  else if (Fp <= 2048)
+    limb_rows_block_kernel<2><<<(unsigned)rows_p, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part,
+                                                                 tau_const, vec);
+  else if (Fp <= 4096)
+    limb_rows_block_kernel<4><<<(unsigned)rows_p, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part,
+                                                                 tau_const, vec);
   else
-    limb_rows_kernel<0><<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const);
+    limb_rows_2pass_kernel<<<grid, warps * 32, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, tau_part, tau_const,
+                                                        vec);
   return cudaGetLastError();
 }
 
@@ -1363,10 +1465,11 @@ cudaError_t launch_tc_round(int mode, const float* src, int64_t rows, int64_t ro
   const int64_t total = rows_p * Fp;
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (ld_src % 4 == 0);
   if (mode == 0)
-    round_rows_kernel<0><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out);
+    round_rows_kernel<0><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, vec);
   else
-    round_rows_kernel<1><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out);
+    round_rows_kernel<1><<<(unsigned)grid, 256, 0, st>>>(src, rows, rows_p, F, ld_src, Fp, out, vec);
   return cudaGetLastError();
 }
 
