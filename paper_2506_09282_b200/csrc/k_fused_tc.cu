@@ -233,19 +233,21 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // float64 re-evaluation of V[row, d] (fixed lane order, warp-cooperative).
 __device__ __forceinline__ float recheck_dot(const float* __restrict__ xr, const float* __restrict__ br,
                                              int64_t F, int lane) {
+  // lane sums f = lane, lane + 32, ... in f order (fixed), then a fixed butterfly; 32
+  // independent loads in flight per chunk of 512 elements (one memory round trip each)
+  constexpr int U = 16;
   double s = 0.0;
-  int64_t f = lane;
-  for (; f + 96 < F; f += 128) {         // 8 independent loads in flight, then the FMAs in f order
-    float xv[4], bv[4];
+  for (int64_t f0 = 0; f0 < F; f0 += 32 * U) {
+    float xv[U], bv[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      xv[u] = __ldg(xr + f + 32 * u);
-      bv[u] = __ldg(br + f + 32 * u);
+    for (int u = 0; u < U; ++u) {
+      const int64_t f = f0 + 32 * u + lane;
+      xv[u] = f < F ? __ldg(xr + f) : 0.f;
+      bv[u] = f < F ? __ldg(br + f) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s = fma((double)xv[u], (double)bv[u], s);
+    for (int u = 0; u < U; ++u) s = fma((double)xv[u], (double)bv[u], s);   // 0 x 0 adds exactly 0
   }
-  for (; f < F; f += 32) s = fma((double)__ldg(xr + f), (double)__ldg(br + f), s);
   s = warp_sum_xor(s);
   return s >= 0.0 ? 1.f : -1.f;
 }
@@ -1487,7 +1489,7 @@ cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, i
 
 cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
                               cudaStream_t st) {
-  tc_recheck_kernel<<<148 * 4, 256, 0, st>>>(o.X, o.Bt, o.F, o.Fp, o.Cp, o.Dp, o.K, tc_kp(o.K), o.flags,
+  tc_recheck_kernel<<<148 * 8, 256, 0, st>>>(o.X, o.Bt, o.F, o.Fp, o.Cp, o.Dp, o.K, tc_kp(o.K), o.flags,
                                              o.flag_count, o.flag_cap, shift, o.corr, o.dirty, o.recheck,
                                              o.hout, o.hout_ldw);
   cudaError_t e = cudaGetLastError();
