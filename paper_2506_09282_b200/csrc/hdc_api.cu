@@ -286,7 +286,15 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   const int mode = tc_mode_of(m);
   hdc_status_t stt = ensure_tc_ws(m, N);
   if (stt != HDC_OK) return stt;
-  const int64_t gm = kTileM * m->cl_n;
+  // one N-tile or less: no CTA pairs over N-tiles (the partner tile would be all padding);
+  // single CTAs spread the D-tiles over all SMs instead
+  int cl_n = m->cl_n, cl_d = m->cl_d, cl_virt = m->cl_virt;
+  if (N <= kTileM && cl_virt != 1) {
+    cl_n = 1;
+    cl_d = 1;
+    cl_virt = 0;
+  }
+  const int64_t gm = kTileM * cl_n;
   const int64_t Np = (N + gm - 1) / gm * gm;
   cudaError_t e;
   if (mode == 2)
@@ -302,9 +310,9 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.Dq = m->Dq;
   o.K = m->K;
   o.N_p = Np;
-  o.cl_n = m->cl_n;
-  o.cl_d = m->cl_d;
-  o.cl_virt = m->cl_virt;
+  o.cl_n = cl_n;
+  o.cl_d = cl_d;
+  o.cl_virt = cl_virt;
   o.A = m->Atc;
   o.B = m->Btc;
   o.Cil = m->Cil;
