@@ -1271,14 +1271,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)p;
-  }
+      return (EncodeTiledFn)p;
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -1314,19 +1314,20 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // persistent: as many clusters as can be co-resident (148 SMs: 74 pairs, 33 quads)
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
-    cfg.gridDim = dim3(CLS * (num_sms / CLS), 1, 1);
+  // persistent: as many clusters as can be co-resident (148 SMs: 74 pairs, 33 quads);
+  // computed once per instantiation (thread-safe static initialisation)
+  static const int max_clusters = [&]() {
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3(CLS * (num_sms / CLS), 1, 1);
     int n = 0;
     if (!HWC) {
       n = num_sms / CLS;                          // one CTA per SM, CLS CTAs per virtual cluster
-    } else if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+    } else if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n < 1) {
       cudaGetLastError();
       n = num_sms / CLS;
     }
-    max_clusters = n;
-  }
+    return n;
+  }();
   p.G = (int)(p.T < max_clusters ? p.T : max_clusters);
   const int64_t per = (p.T + p.G - 1) / p.G;    // cluster tiles per range (at most)
   p.nslot = (CLD == 1) ? 2 : (int)((per + p.TdG - 1) / p.TdG + 1);

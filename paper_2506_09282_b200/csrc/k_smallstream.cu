@@ -19,6 +19,7 @@
 //
 // HDC_PREC_FP32 sign exactness: |v| <= tau = c_F ||x_n|| ||b_d|| is re-evaluated in
 // float64 (warp-cooperative, fixed order), as in the other fp32 kernels.
+#include <atomic>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -448,8 +449,8 @@ cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
   const size_t sm = stream_smem(nst, p.F, NB, p.K, p.max_cols);
   if (sm > lim) return cudaErrorInvalidValue;
   p.nst = nst;
-  static size_t attr_set = 0;                   // host-side attribute call only when it grows
-  if (sm > attr_set) {
+  static std::atomic<size_t> attr_set{0};      // host-side attribute call only when it grows
+  if (sm > attr_set.load()) {
     cudaError_t e = cudaFuncSetAttribute(smallstream_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lim);
     if (e != cudaSuccess) return e;
