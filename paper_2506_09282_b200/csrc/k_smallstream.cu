@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   for (int i = lane; i < NB * K; i += 32) sw[i] = 0.f;
   cbar();
   mbar_wait(xfull, 0);
+  // zero rows nrows..NB-1 (also overwrites the bulk copy's tail slack past row nrows-1)
+  for (int i = p.nrows * F + tid; i < NB * F; i += kCt) Xraw[xoff + i] = 0.f;
   for (int n = warp; n < p.nrows; n += kCw) {
     float ss = 0.f;
     for (int f = lane; f < F; f += 32) ss = fmaf(Xs[n * F + f], Xs[n * F + f], ss);
@@ -213,7 +215,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
         const float* xc = Xs + f0 + r;                // column f of X: Xs[n F + f]
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
-          const float x = n < p.nrows ? xc[n * F] : 0.f;
+          const float x = *xc;                        // rows >= nrows are zero
+          xc += F;
           acc2[n * 2 + 0] = ffma2(x, b01, acc2[n * 2 + 0]);   // each lane: fmaf(x, b_q, acc)
           acc2[n * 2 + 1] = ffma2(x, b23, acc2[n * 2 + 1]);
         }
