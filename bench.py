@@ -239,6 +239,10 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
     if ceiling:
         out["path_ceiling"] = ceiling
         out["frac_of_path_ceiling"] = achieved / ceiling
+    if bound == "tensor":
+        # binding resource of the fused tcgen05 kernel: per K stage the MMA
+        # operand reads plus the TMA writes pass the 128 B/clk/SM shared-memory port
+        out["limit"] = "shared-memory bandwidth (MMA operand reads + TMA writes), DESIGN.md §11"
     return out
 
 
