@@ -1,0 +1,1 @@
+timeout 200 python tools/e2e_probe.py 2>&1 | grep -v "^\[hdc"
