@@ -1,11 +1,11 @@
 // k_fused_tc.cu -- K4: fused large-batch HDC inference on the 5th-gen tensor
 // cores (tcgen05 + TMEM + TMA), sm_100a.
 //
-// Alg. 1 per (N-tile of 128 rows) x (D-tile of 80 columns):
+// Alg. 1 per (N-tile of 128 rows) x (D-tile of BN columns):
 //   Stage I   V_tile = X_tile B_tile: tcgen05.mma, accumulators in TMEM
 //             (eq. batch_encode);
 //   act       HardSign in the epilogue warps after tcgen05.ld, written
-//             as exact bf16 +-1 into a shared-memory H tile;
+//             as exact bf16 +-1 into TMEM (bf16/tf32) or a shared-memory H tile (int8);
 //   Stage II  S[n, :] += H_tile C_tile^T as a second tcgen05.mma (bf16, C split
 //             into hi + lo bf16 parts) into a TMEM accumulator that lives for the
 //             CTA's whole run of D-tiles of one N-tile (eq. batch_sim P:180-183;
@@ -13,24 +13,28 @@
 // H never leaves the SM.
 //
 // Precision modes (hdc_precision_t):
-//   BF16  X, B rounded to bf16 (RN); kind::f16, fp32 accumulate.
-//   TF32  X, B rounded to tf32 (RNA); kind::tf32, fp32 accumulate.
+//   BF16  X, B rounded to bf16 (RN); kind::f16, fp32 accumulate; BN = 160.
+//   TF32  X, B rounded to tf32 (RNA); kind::tf32, fp32 accumulate; BN = 160.
 //   INT8x3 (HDC_PREC_FP32_TC, sign-exact): per-row/column scaled 21-bit integer
 //         images of X and B split into three balanced base-128 int8 limbs; the
-//         six limb products with i + j <= 2 run as kind::i8 MMAs with EXACT int32
-//         accumulation into three TMEM accumulators, combined in int64.  The
-//         rigorous bound of that integer image flags the few
-//         |I| <= tau, re-evaluated in float64 -> every HardSign decision equals
-//         that of the exact product X B.
+//         six limb products with i + j <= 2 run as three N-concatenated kind::i8
+//         MMAs with EXACT int32 accumulation into three TMEM accumulators (BN = 80),
+//         combined in int64.  The rigorous bound of that integer image (DESIGN.md
+//         §4) flags the few |I| <= tau; they are re-evaluated in float64 after the
+//         kernel (tc_recheck_kernel), so every HardSign decision equals that of
+//         the exact product X B and S is corrected exactly where a sign flips.
 //
-// Warp roles (384 threads, one CTA per SM, persistent over a contiguous range
-// of the n-major tile sequence): warp 0 TMA producer, warp 1 MMA issuer (and
-// TMEM owner), warps 4..11 epilogue (warp w reads TMEM lanes 32*(w%4).. and
-// column half (w-4)/4).  smem: 4-stage ring of SWIZZLE_64B K-major operand
-// tiles, 2 H tiles, 2 C tiles (interleaved K-major bf16 hi/lo); TMEM: two
-// Stage I accumulator buffers + the Stage II accumulator.  Partial scores of
-// N-tiles split between CTAs are summed in CTA order by the last-arriving CTA,
-// which takes the lowest-index argmax: bit-deterministic.
+// Warp roles (384 threads, one CTA per SM, persistent over a contiguous range of the
+// n-major tile sequence): warp 0 TMA producer, warp 1 Stage I MMA issuer (TMEM
+// owner), warp 2 C-tile producer, warp 3 Stage II MMA issuer, warps 4..11 epilogue.
+// Operand ring: SWIZZLE_128B K-major stages (64-byte SWIZZLE_64B int8 stages when
+// Fp % 128 != 0).  Clusters: 2x1 CTAs sharing each B tile by TMA multicast (default),
+// single CTAs for one N-tile, virtual 1 x 4 / 1 x 8 groups when the live X tiles plus
+// B exceed L2, or a cta_group::2 pair (HDC_TC_CLUSTER=2x1p).  Both precisions run at
+// the shared-memory bandwidth bound: MMA operand reads + TMA writes per stage at
+// 128 B/clk/SM.  Partial scores of N-tiles split between clusters are
+// summed in a fixed order by the last arriver, which takes the lowest-index argmax:
+// bit-deterministic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
