@@ -240,9 +240,8 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
         out["path_ceiling"] = ceiling
         out["frac_of_path_ceiling"] = achieved / ceiling
     if bound == "tensor":
-        # binding resource of the fused tcgen05 kernel: per K stage the MMA
-        # operand reads plus the TMA writes pass the 128 B/clk/SM shared-memory port
-        out["limit"] = "shared-memory bandwidth (MMA operand reads + TMA writes), DESIGN.md §11"
+        # what the fused tcgen05 kernel spends beyond the MMA floor
+        out["limit"] = "MMA floor per K stage + ~2000 cycles per tile (epilogue/Stage II/TMA interference), DESIGN.md §11"
     return out
 
 

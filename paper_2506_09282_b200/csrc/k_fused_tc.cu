@@ -30,9 +30,9 @@
 // Operand ring: SWIZZLE_128B K-major stages (64-byte SWIZZLE_64B int8 stages when
 // Fp % 128 != 0).  Clusters: 2x1 CTAs sharing each B tile by TMA multicast (default),
 // single CTAs for one N-tile, virtual 1 x 4 / 1 x 8 groups when the live X tiles plus
-// B exceed L2, or a cta_group::2 pair (HDC_TC_CLUSTER=2x1p).  Both precisions run at
-// the shared-memory bandwidth bound: MMA operand reads + TMA writes per stage at
-// 128 B/clk/SM.  Partial scores of N-tiles split between clusters are
+// B exceed L2, or a cta_group::2 pair (HDC_TC_CLUSTER=2x1p).  Time per tile = the MMA
+// floor of its K stages + ~2000 cycles the pipeline does not hide (epilogue TMEM traffic,
+// Stage II, operand TMA).  Partial scores of N-tiles split between clusters are
 // summed in a fixed order by the last arriver, which takes the lowest-index argmax:
 // bit-deterministic.
 #include <cuda.h>
