@@ -645,6 +645,20 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
   const int64_t per = (N + nchunks - 1) / nchunks;
   const int b = m->xbuf;
   m->xbuf ^= 1;
+  // Results go straight into mapped pinned host buffers when the caller's are (the kernels
+  // write them over PCIe): no device-to-host copy on the copy engine, which on some
+  // systems serves both directions in one queue -- a small label copy would then wait
+  // behind the next call's host-to-device copy and stall the compute stream.
+  auto mapped = [](void* h) -> void* {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+  };
+  int32_t* lab_map = static_cast<int32_t*>(mapped(labels_host));
+  float* sc_map = scores_host ? static_cast<float*>(mapped(scores_host)) : nullptr;
   float* xd = m->Xdev + (int64_t)b * m->Xdev_rows * m->F;
   HDC_CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->ev_done[b], 0), "stream wait");
   // (same stream: a no-op; another stream: the device labels / scores are not reused early)
@@ -658,13 +672,15 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                  "H2D X");
     HDC_CUDA_TRY(cudaEventRecord(m->ev_h2d[i], m->copy_stream), "event record");
     HDC_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_h2d[i], 0), "stream wait");
-    st = run(m, xd + r0 * m->F, n, m->ldev + r0, scores_host ? m->sdev + r0 * m->K : nullptr,
-             HDC_PATH_AUTO, s);
+    int32_t* lab = lab_map ? lab_map + r0 : m->ldev + r0;
+    float* sc = scores_host ? (sc_map ? sc_map + r0 * m->K : m->sdev + r0 * m->K) : nullptr;
+    st = run(m, xd + r0 * m->F, n, lab, sc, HDC_PATH_AUTO, s);
     if (st != HDC_OK) return st;
     launches += m->last_launches;
-    HDC_CUDA_TRY(cudaMemcpyAsync(labels_host + r0, m->ldev + r0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s),
-                 "D2H labels");
-    if (scores_host)
+    if (!lab_map)
+      HDC_CUDA_TRY(cudaMemcpyAsync(labels_host + r0, m->ldev + r0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s),
+                   "D2H labels");
+    if (scores_host && !sc_map)
       HDC_CUDA_TRY(cudaMemcpyAsync(scores_host + r0 * m->K, m->sdev + r0 * m->K, sizeof(float) * n * m->K,
                                    cudaMemcpyDeviceToHost, s),
                    "D2H scores");
