@@ -117,7 +117,9 @@ hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int3
  * (rows are independent, so results equal the one-shot call).
  * Ordering: the copies of X_host are ordered after this model's previous host-path
  * calls, NOT after other work already queued on `stream` -- X_host must be fully
- * written when the call is made.  Labels / scores are written in `stream` order.
+ * written when the call is made.  Labels / scores are written in `stream` order:
+ * directly by the kernels when the host buffers are mapped pinned memory (cudaHostAlloc,
+ * or any pinned allocation under unified addressing), else by device-to-host copies.
  * Host buffers should be pinned (cudaHostAlloc) for the copies to be
  * asynchronous; the call returns after enqueue -- synchronise `stream` before
  * reading the outputs or reusing X_host.  Concurrent host-path calls on the same
