@@ -19,7 +19,13 @@
 namespace hdc {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+#ifndef HDC_K3_BK
+#define HDC_K3_BK 16
+#endif
+#ifndef HDC_K3_STAGES
+#define HDC_K3_STAGES 4
+#endif
+constexpr int BM = 128, BN = 128, BK = HDC_K3_BK, STAGES = HDC_K3_STAGES, THREADS = 256;
 constexpr int HS = BM + 4;           // Hs row stride (floats)
 constexpr int LIST_CAP = 1024;       // flagged-element list per tile
 constexpr int kSaccSmemMaxK = 64;    // larger K keeps the score accumulator in L2
@@ -137,8 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
     float* bs = Bs + stage * BK * BN;
     const float* xa = Xtile + f0 * BM;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int q = t + THREADS * u;       // float4 index 0..511
+    for (int u = 0; u < BK * BM / 4 / THREADS; ++u) {
+      const int q = t + THREADS * u;       // float4 index 0..BK*32-1
       cp_async16(as + 4 * q, xa + 4 * q);
       const int row = q >> 5, c4 = q & 31;
       cp_async16(bs + row * BN + 4 * c4, p.Bp + (f0 + row) * p.Dp + d0 + 4 * c4);
@@ -151,11 +157,14 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
     cp_async_commit();
   }
 
-  float acc[8][8];
+  // 8 x 8 outputs as float2 pairs (b, b + 1): FFMA2, two FMAs per instruction, each
+  // element still accumulated in k order
+  float2 acc2[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+    for (int b = 0; b < 4; ++b) acc2[a][b] = make_float2(0.f, 0.f);
+#define ACC(a, b) (((b) & 1) ? acc2[a][(b) >> 1].y : acc2[a][(b) >> 1].x)
 
   for (int it = 0; it < total; ++it) {
     cp_async_wait<STAGES - 2>();
@@ -174,11 +183,12 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
       const float4 b0 = *reinterpret_cast<const float4*>(bs + k * BN + tx * 4);
       const float4 b1 = *reinterpret_cast<const float4*>(bs + k * BN + 64 + tx * 4);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float2 bp[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < 4; ++b) acc2[a][b] = ffma2(av[a], bp[b], acc2[a][b]);
     }
 
     if (it % KS == KS - 1) {
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
         float h[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-          const float v = acc[a][b];
+          const float v = ACC(a, b);
           h[a] = hardsign(v);
           const int r = a < 4 ? ty * 4 + a : 64 + ty * 4 + a - 4;
           if (p.recheck && fabsf(v) <= p.tau_coef * xn[a] * bn[b] + kSignBoundAbs &&
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_ffma_kernel(const FusedParam
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+        for (int b = 0; b < 4; ++b) acc2[a][b] = make_float2(0.f, 0.f);
       __syncthreads();
       const int nl = min(s_nlist, LIST_CAP);
       for (int q = warp; q < nl; q += THREADS / 32) {
