@@ -163,3 +163,25 @@ def test_host_path_pipelined_calls(hdc, prec):
         clear = (top2[:, 1] - top2[:, 0]) > 1e-2
         assert np.array_equal(yh.numpy()[clear], y[clear])
     m.close()
+
+
+def test_host_path_pageable_outputs(hdc):
+    # non-pinned (pageable) label / score buffers take the device-to-host copy path; pinned
+    # ones are written directly by the kernels -- both must give the device-call results
+    rng = np.random.default_rng(9)
+    F, D, K, N = 50, 1500, 5, 300
+    B = rng.standard_normal((F, D)).astype(np.float32)
+    C = rng.standard_normal((K, D)).astype(np.float32)
+    X = rng.uniform(-1, 1, (N, F)).astype(np.float32)
+    Bd, Cd = to_dev(B, C)
+    m = hdc.Model(Bd, Cd, prec="fp32_tc")
+    y, S = run_model(m, X, "auto")
+    Xh = torch.from_numpy(X).pin_memory()
+    yp, Sp = torch.empty(N, dtype=torch.int32), torch.empty(N, K, dtype=torch.float32)   # pageable
+    m.infer_host(Xh, yp, Sp)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(Sp.numpy(), S, rtol=1e-5, atol=1e-3)
+    top2 = np.sort(S, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 1e-2
+    assert np.array_equal(yp.numpy()[clear], y[clear])
+    m.close()
