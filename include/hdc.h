@@ -63,7 +63,9 @@ typedef enum {
  *     int8 limbs; the six limb products of weight >= 2^-14 accumulate EXACTLY
  *     in int32 (tcgen05 kind::i8); every pre-activation within the rigorous
  *     bound of that image is re-evaluated in float64 -> HardSign decisions
- *     equal those of the exact product.  Stage II in fp32 FMA.
+ *     equal those of the exact product.  Stage II on tcgen05 with
+ *     C split into bf16 hi + lo (fp32 accumulation); where a re-evaluated sign
+ *     differs from the provisional one, S is corrected exactly (int64 fixed point).
  *     Falls back to the HDC_PREC_FP32 kernels (same guarantee) when K > 32 or
  *     F > 100000.  Low-precision modes fall back likewise when K > 64. */
 typedef enum {
