@@ -4,7 +4,6 @@ fp32_tc (int8x3 limbs + fp64 recheck) must meet the fp32 policy; tf32/bf16 the
 low-precision policy (scores within 1e-2 of ||C_k||_1, agreement reported)."""
 import numpy as np
 import pytest
-import torch
 
 import oracle
 from oracle.policy import check_fp32, check_lowp

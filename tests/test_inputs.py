@@ -65,7 +65,6 @@ def test_config_tensors():
 
 @pytest.mark.gpu
 def test_device_generator_matches_host(cuda_device):
-    import torch
     from hdc_inputs.device import uniform_f32_device
     for (s, c, a, b) in [(0, 1, -1.0, 1.0), (3, 1001, -1.0, 1.0), (617 * 5, 617 * 33, 0.0, 1.0)]:
         dev = uniform_f32_device(0, 0, s, c, a, b, cuda_device).cpu().numpy()
