@@ -143,8 +143,10 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
  * `world` pointers: the exchange buffer of each rank, mapped into this process (CUDA IPC
  * / symmetric memory; xbufs[rank] is this rank's own).  Each buffer holds
  * hdc_dshard_exchange_bytes(N, K, world) bytes (world uint32 signal words, padded to 16
- * bytes, then 2 x world slots of N*K floats) and must be zeroed once before the first
- * call (epoch 1 is the first valid epoch; the buffer may serve any N up to its size).  The small-batch kernel's last CTA stores this
+ * bytes, then 2 x world slots of 32*K floats: slots are sized for the largest N, so one
+ * buffer serves every 1 <= N <= 32 and N may change from call to call) and must be zeroed
+ * once before the first call (epoch 1 is the first valid epoch).  The N argument of
+ * hdc_dshard_exchange_bytes is only validated (0 is returned outside 1..32).  The small-batch kernel's last CTA stores this
  * rank's partial scores into every rank's buffer (peer stores), release-signals them,
  * waits until all ranks' partials arrived and sums them in rank order, so labels and
  * scores (N*K, optional) are identical on every rank.  One launch, no NCCL.  The ranks'
@@ -200,6 +202,14 @@ int64_t hdc_model_recheck_count(hdc_model_t m);
 
 /* Number of kernel launches the last call on this model enqueued. */
 int32_t hdc_model_last_launch_count(hdc_model_t m);
+
+/* Kernel family that computed the last call on this model (diagnostic; -1 on a NULL
+ * model).  The arithmetic differs by family, which is what the parity tests key on:
+ *   HDC_KERNEL_SMALL: fp32 streaming D-split kernel (sign-exact, any precision's model);
+ *   HDC_KERNEL_FFMA:  fp32 fused FFMA kernel (sign-exact);
+ *   HDC_KERNEL_TC:    fused tcgen05 kernel in the model's precision. */
+typedef enum { HDC_KERNEL_NONE = 0, HDC_KERNEL_SMALL = 1, HDC_KERNEL_FFMA = 2, HDC_KERNEL_TC = 3 } hdc_kernel_t;
+int32_t hdc_model_last_kernel(hdc_model_t m);
 
 /* Diagnostics for roofline reporting: when enabled, each call records CUDA
  * events on its stream around its dominant kernel (the fused kernel, or the

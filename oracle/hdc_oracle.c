@@ -37,6 +37,37 @@ static int all_finite(const float* a, int64_t n) {
 /* HardSign: +1 if x >= 0 else -1.  -0.0 >= 0.0 is true -> +1. */
 double oracle_hardsign(double x) { return x >= 0.0 ? 1.0 : -1.0; }
 
+/* Operand formats of the low-precision paths (not in the paper, which is fp32-only,
+ * P:143; the TF32 / BF16 paths are BASELINE north_star's additions, DESIGN.md
+ * reading R15).  Both keep fp32's 8-bit exponent and shorten the significand:
+ *   ORACLE_FMT_TF32: 10 explicit mantissa bits, round to nearest, ties AWAY from zero;
+ *   ORACLE_FMT_BF16:  7 explicit mantissa bits, round to nearest, ties to EVEN.
+ * Definition: for x != 0 with 2^(e-1) <= |x| < 2^e (frexp), the representable
+ * neighbours are the multiples of q = 2^(e-1-p) (p = explicit bits; q >= 2^(-126-p)
+ * below the normal range); the result is q * round(x / q).  x / q is exact in double. */
+#define ORACLE_FMT_FP32 0
+#define ORACLE_FMT_TF32 1
+#define ORACLE_FMT_BF16 2
+double oracle_round_fmt(double x, int fmt) {
+  if (fmt == ORACLE_FMT_FP32 || x == 0.0 || !isfinite(x)) return x;
+  const int p = (fmt == ORACLE_FMT_TF32) ? 10 : 7;
+  int e;
+  frexp(x, &e);
+  int qe = e - 1 - p;
+  if (qe < -126 - p) qe = -126 - p;
+  const double q = ldexp(1.0, qe);
+  const double t = x / q;                      /* exact: a power-of-two scaling */
+  double r;
+  if (fmt == ORACLE_FMT_TF32) {
+    r = round(t);                              /* C99 round(): halfway cases away from zero */
+  } else {
+    r = floor(t);                              /* nearest, ties to even */
+    const double frac = t - r;
+    if (frac > 0.5 || (frac == 0.5 && fmod(r, 2.0) != 0.0)) r += 1.0;
+  }
+  return r * q;
+}
+
 /* Pre-activation V = X B for rows [0,N): V[n,d] = sum_f X[n,f] * B[f,d]
  * (eq. nonlinenc: bind x_i to b_i, bundle over i).  Loop n -> f -> d. */
 int oracle_preact(const float* X, const float* B, int64_t N, int64_t F, int64_t D, double* V) {
@@ -64,11 +95,47 @@ int oracle_preact(const float* X, const float* B, int64_t N, int64_t F, int64_t 
  *   namb   [N] nullable: |A64(n)|
  *   nthreads: OpenMP threads over rows (<=0: runtime default).  Rows are
  *          independent, so the result does not depend on it. */
+int oracle_infer_ex(const float* X, const float* B, const float* C, int64_t N, int64_t F, int64_t D,
+                    int64_t K, int fmt, double gamma, double* S, int32_t* y, double* allow,
+                    int32_t* namb, int nthreads);
+
 int oracle_infer(const float* X, const float* B, const float* C, int64_t N, int64_t F, int64_t D,
                  int64_t K, double* S, int32_t* y, double* allow, int32_t* namb, int nthreads) {
+  return oracle_infer_ex(X, B, C, N, F, D, K, ORACLE_FMT_FP32, (double)(F + 1) * ldexp(1.0, -53),
+                         S, y, allow, namb, nthreads);
+}
+
+/* Generalised form (test infrastructure for the TF32 / BF16 paths, R15, R16):
+ *   fmt   ORACLE_FMT_FP32: X and B as given (the paper's fp32 operands).
+ *         ORACLE_FMT_TF32 / ORACLE_FMT_BF16: every element of X and B is first rounded
+ *         to that format (oracle_round_fmt), then Alg. 1 runs unchanged in float64 on
+ *         the rounded operands; C is not rounded.
+ *   gamma the ambiguity set is A(n) = { d : W[n,d] > 0, |V[n,d]| <= gamma W[n,d] }, with
+ *         V and W = sum_f |x||b| both of the (rounded) operands; allow[n,k] =
+ *         sum_{d in A(n)} 2|C[k,d]| (the score movement of flipping every sign in A). */
+int oracle_infer_ex(const float* X, const float* B, const float* C, int64_t N, int64_t F, int64_t D,
+                    int64_t K, int fmt, double gamma, double* S, int32_t* y, double* allow,
+                    int32_t* namb, int nthreads) {
   if (N < 0 || F < 1 || D < 1 || K < 1) return 2;
+  if (fmt != ORACLE_FMT_FP32 && fmt != ORACLE_FMT_TF32 && fmt != ORACLE_FMT_BF16) return 2;
   if (!all_finite(X, N * F) || !all_finite(B, F * D) || !all_finite(C, K * D)) return 1;
-  const double amb_c = (double)(F + 1) * ldexp(1.0, -53);
+  const double amb_c = gamma;
+  /* the operands Stage I sees: rounded copies when fmt asks for them */
+  float* Xr = NULL;
+  float* Br = NULL;
+  if (fmt != ORACLE_FMT_FP32) {
+    Xr = (float*)malloc(sizeof(float) * (size_t)(N * F > 0 ? N * F : 1));
+    Br = (float*)malloc(sizeof(float) * (size_t)(F * D));
+    if (!Xr || !Br) {
+      free(Xr);
+      free(Br);
+      return 3;
+    }
+    for (int64_t i = 0; i < N * F; ++i) Xr[i] = (float)oracle_round_fmt((double)X[i], fmt);
+    for (int64_t i = 0; i < F * D; ++i) Br[i] = (float)oracle_round_fmt((double)B[i], fmt);
+    X = Xr;
+    B = Br;
+  }
   int err = 0;
 #ifdef _OPENMP
   if (nthreads <= 0) nthreads = omp_get_max_threads();
@@ -124,7 +191,16 @@ int oracle_infer(const float* X, const float* B, const float* C, int64_t N, int6
     free(v);
     free(w);
   }
+  free(Xr);
+  free(Br);
   return err;
+}
+
+/* Element-wise oracle_round_fmt over an fp32 array (out may alias in). */
+int oracle_round_array(const float* in, int64_t n, int fmt, float* out) {
+  if (fmt != ORACLE_FMT_FP32 && fmt != ORACLE_FMT_TF32 && fmt != ORACLE_FMT_BF16) return 2;
+  for (int64_t i = 0; i < n; ++i) out[i] = (float)oracle_round_fmt((double)in[i], fmt);
+  return 0;
 }
 
 int oracle_num_threads(void) {

@@ -101,6 +101,7 @@ struct hdc_model_s {
   cudaStream_t copy_stream = nullptr;   // host-buffer path: H2D copies, overlapped with compute
   cudaEvent_t ev_h2d[8] = {};
   int32_t last_launches = 0;
+  int32_t last_kernel = 0;        // hdc_kernel_t of the last call's dominant kernel
   // diagnostics: CUDA events around the dominant kernel of each call
   bool timing = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -340,6 +341,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   m->toc(st);
   if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
   m->last_launches = 2;
+  m->last_kernel = HDC_KERNEL_TC;
   if (mode == 2) {
     e = launch_tc_recheck(o, N, S, labels, m->corr_shift, st);
     if (e != cudaSuccess) return cuda_fail(e, "tc recheck launch");
@@ -369,6 +371,7 @@ hdc_status_t run_fused(hdc_model_s* m, const float* X, int64_t N, int32_t* label
   m->toc(st);
   if (e != cudaSuccess) return cuda_fail(e, "fused_ffma launch");
   m->last_launches = 2;
+  m->last_kernel = HDC_KERNEL_FFMA;
   return HDC_OK;
 }
 
@@ -376,6 +379,7 @@ hdc_status_t run_fused(hdc_model_s* m, const float* X, int64_t N, int32_t* label
 hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, float* scores,
                  hdc_path_t path, cudaStream_t st) {
   m->last_launches = 0;
+  m->last_kernel = HDC_KERNEL_NONE;
   if (N == 0) return HDC_OK;
   const ModelView mv = m->view();
   const bool recheck = (m->prec == HDC_PREC_FP32 || m->prec == HDC_PREC_FP32_TC ||
@@ -403,6 +407,7 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
                                             labels ? labels + r0 : nullptr, recheck, m->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "smallbatch launch");
     ++m->last_launches;
+    m->last_kernel = HDC_KERNEL_SMALL;
   }
   m->toc(st);
   return HDC_OK;
@@ -564,8 +569,10 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
 }
 
 int64_t hdc_dshard_exchange_bytes(int64_t N, int64_t K, int world) {
-  if (N < 1 || K < 1 || world < 1) return 0;
-  const int64_t stride = (N * K + 3) / 4 * 4, sigpad = (world + 3) / 4 * 4;
+  if (N < 1 || N > kDshardMaxRows || K < 1 || K > HDC_MAX_K || world < 1) return 0;
+  // slots sized for kDshardMaxRows rows: one buffer serves every N <= 32, and the slot
+  // offsets do not move when N changes between calls
+  const int64_t stride = dshard_slot_floats(K), sigpad = (world + 3) / 4 * 4;
   return (int64_t)4 * (sigpad + 2 * world * stride);
 }
 
@@ -592,6 +599,7 @@ hdc_status_t hdc_model_infer_dshard(hdc_model_t m, const float* X, int64_t N, in
   m->toc(s);
   if (e != cudaSuccess) return cuda_fail(e, "D-shard small-batch launch");
   m->last_launches = 1;
+  m->last_kernel = HDC_KERNEL_SMALL;
   return HDC_OK;
 }
 
@@ -779,6 +787,8 @@ int64_t hdc_model_recheck_count(hdc_model_t m) {
 }
 
 int32_t hdc_model_last_launch_count(hdc_model_t m) { return m ? m->last_launches : -1; }
+
+int32_t hdc_model_last_kernel(hdc_model_t m) { return m ? m->last_kernel : -1; }
 
 hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");

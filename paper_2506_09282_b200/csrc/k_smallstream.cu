@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
     // Parity double-buffering: a rank writes slot parity e & 1 of call e only after it
     // received every rank's call e-1 signal, i.e. after they finished reading call e-2.
     const int W = p.xworld, par = (int)(p.xepoch & 1u);
-    const int xstride = (nk + 3) & ~3, sigpad = (W + 3) & ~3;
+    const int xstride = (int)dshard_slot_floats(K), sigpad = (W + 3) & ~3;   // N-independent slots
     for (int r = 0; r < W; ++r) {
       float* dst = p.xbufs[r] + sigpad + ((size_t)par * W + p.xrank) * xstride;
       for (int i = tid; i < nk; i += kCt) dst[i] = Sfin[i];

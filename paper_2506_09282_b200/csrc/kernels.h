@@ -41,6 +41,10 @@ cudaError_t launch_smallbatch(const ModelView& m, const SmallWorkspace& ws, cons
 // K2s (k_smallstream.cu): TMA-streamed small-batch kernel, rows [0, n), n <= 32.
 bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms);
 // In-kernel D-shard exchange of the small-batch kernel (hdc_model_infer_dshard).
+// Slots are sized for kDshardMaxRows rows whatever the call's N, so the slot offsets of
+// consecutive calls never depend on N (a rank may run call e+1 while a peer still sums e).
+constexpr int kDshardMaxRows = 32;
+__host__ __device__ inline int64_t dshard_slot_floats(int64_t K) { return (kDshardMaxRows * K + 3) / 4 * 4; }
 struct DshardExchange {
   float* const* bufs;   // device array [world] of the ranks' exchange buffers
   int rank, world;

@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("HDC_LIB_PATH") or os.path.join(
 
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp32_tc": 3}
 PATH = {"auto": 0, "small": 1, "fused": 2}
+KERNELS = {0: "none", 1: "small", 2: "ffma", 3: "tc"}
 _STATUS = {0: "HDC_OK", 1: "HDC_ERR_INVALID_VALUE", 2: "HDC_ERR_MISALIGNED",
            3: "HDC_ERR_UNSUPPORTED", 4: "HDC_ERR_NO_MEMORY", 5: "HDC_ERR_CUDA"}
 
@@ -53,6 +54,8 @@ def lib():
         L.hdc_model_recheck_count.restype = I64
         L.hdc_model_last_launch_count.argtypes = [P]
         L.hdc_model_last_launch_count.restype = ctypes.c_int32
+        L.hdc_model_last_kernel.argtypes = [P]
+        L.hdc_model_last_kernel.restype = ctypes.c_int32
         L.hdc_model_set_kernel_timing.argtypes = [P, I32]
         L.hdc_model_set_kernel_timing.restype = I32
         L.hdc_model_last_kernel_ms.argtypes = [P]
@@ -92,6 +95,32 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _rows(X, F, name="X"):
+    """X must be a 2-D (N x F) CUDA float32 tensor; returns it contiguous."""
+    X = _dev_f32(X, name)
+    if X.dim() != 2 or X.shape[1] != F:
+        raise ValueError("%s must be N x F = ? x %d, got %s" % (name, F, tuple(X.shape)))
+    return X
+
+
+def _out(t, dtype, numel, device, name):
+    """A caller-supplied output: right dtype, contiguous, >= numel elements, on `device`
+    (a torch.device: CUDA for the device entry points, CPU for the host one).  The C
+    layer writes numel elements through the raw pointer, so a short or strided tensor
+    would be overrun -- reject it instead."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("%s must be a torch tensor" % name)
+    if t.dtype != dtype:
+        raise TypeError("%s must be %s, got %s" % (name, dtype, t.dtype))
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    if t.numel() < numel:
+        raise ValueError("%s has %d elements, needs %d" % (name, t.numel(), numel))
+    if t.device.type != device.type or (device.type == "cuda" and t.device != device):
+        raise ValueError("%s must be on %s, is on %s" % (name, device, t.device))
+    return t
+
+
 class Model:
     """A resident model (hdc_model_create): B (F x D) and C (K x D) on the device."""
 
@@ -115,14 +144,10 @@ class Model:
 
     def infer(self, X, labels=None, scores=None, path="auto", stream=None, return_scores=False):
         """Labels (int32 N) and optionally scores (fp32 N x K) for X (N x F)."""
-        X = _dev_f32(X, "X")
-        if X.dim() != 2 or X.shape[1] != self.F:
-            raise ValueError("X must be N x F")
+        X = _rows(X, self.F)
         N = X.shape[0]
-        if labels is None:
-            labels = torch.empty(N, dtype=torch.int32, device=X.device)
-        if scores is None and return_scores:
-            scores = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        labels = self._labels(labels, N, X.device)
+        scores = self._scores(scores, return_scores, N, X.device)
         with torch.cuda.device(self.device):
             _check(lib().hdc_model_infer_path(self._h, _ptr(X), N, _ptr(labels), _ptr(scores),
                                               PATH[path], _stream_ptr(stream, X.device)))
@@ -130,11 +155,14 @@ class Model:
 
     def encode(self, X, H=None, stream=None):
         """Stage I only: bit-packed H (N x ceil(D/32) int32 words; bit set <=> h = -1)."""
-        X = _dev_f32(X, "X")
+        X = _rows(X, self.F)
         N = X.shape[0]
         ldw = (self.D + 31) // 32
         if H is None:
             H = torch.empty(N, ldw, dtype=torch.int32, device=X.device)
+        elif H.dim() != 2 or H.shape[0] != N or H.shape[1] < ldw:
+            raise ValueError("H must be N x (>= ceil(D/32)) int32 words")
+        _out(H, torch.int32, N * ldw, X.device, "H")
         with torch.cuda.device(self.device):
             _check(lib().hdc_model_encode(self._h, _ptr(X), N, _ptr(H), H.shape[1],
                                           _stream_ptr(stream, X.device)))
@@ -144,7 +172,13 @@ class Model:
         """End-to-end call on (pinned) host tensors; asynchronous on `stream`."""
         if X_host.is_cuda or X_host.dtype != torch.float32 or not X_host.is_contiguous():
             raise TypeError("X_host must be a contiguous host float32 tensor")
+        if X_host.dim() != 2 or X_host.shape[1] != self.F:
+            raise ValueError("X_host must be N x F = ? x %d" % self.F)
         N = X_host.shape[0]
+        cpu = torch.device("cpu")
+        _out(labels_host, torch.int32, N, cpu, "labels_host")
+        if scores_host is not None:
+            _out(scores_host, torch.float32, N * self.K, cpu, "scores_host")
         with torch.cuda.device(self.device):
             _check(lib().hdc_model_infer_host(self._h, _ptr(X_host), N, _ptr(labels_host),
                                               _ptr(scores_host), _stream_ptr(stream, self.device)))
@@ -152,10 +186,11 @@ class Model:
 
     def partial_scores(self, X, out=None, stream=None):
         """Scores over this model's D-slice, no argmax (D-shard piece, Alg. 3)."""
-        X = _dev_f32(X, "X")
+        X = _rows(X, self.F)
         N = X.shape[0]
         if out is None:
             out = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        _out(out, torch.float32, N * self.K, X.device, "out")
         with torch.cuda.device(self.device):
             _check(lib().hdc_model_partial_scores(self._h, _ptr(X), N, _ptr(out),
                                                   _stream_ptr(stream, X.device)))
@@ -166,26 +201,38 @@ class Model:
         """D-shard inference with the cross-rank sum inside the kernel
         (hdc_model_infer_dshard): `xbufs` is a CUDA int64 tensor of the `world` exchange
         buffer addresses (this rank's D-slice model; same X, N <= 32 and epoch on all ranks)."""
-        X = _dev_f32(X, "X")
+        X = _rows(X, self.F)
         if not (isinstance(xbufs, torch.Tensor) and xbufs.is_cuda and xbufs.dtype == torch.int64
-                and xbufs.numel() == world):
-            raise TypeError("xbufs must be a CUDA int64 tensor of `world` addresses")
+                and xbufs.numel() == world and xbufs.is_contiguous()):
+            raise TypeError("xbufs must be a contiguous CUDA int64 tensor of `world` addresses")
         N = X.shape[0]
-        if labels is None:
-            labels = torch.empty(N, dtype=torch.int32, device=X.device)
-        if scores is None and return_scores:
-            scores = torch.empty(N, self.K, dtype=torch.float32, device=X.device)
+        labels = self._labels(labels, N, X.device)
+        scores = self._scores(scores, return_scores, N, X.device)
         with torch.cuda.device(self.device):
             _check(lib().hdc_model_infer_dshard(self._h, _ptr(X), N, _ptr(labels), _ptr(scores), _ptr(xbufs),
                                                 int(rank), int(world), int(epoch) & 0xFFFFFFFF,
                                                 _stream_ptr(stream, X.device)))
         return labels, scores
 
+    def _labels(self, labels, N, device):
+        if labels is None:
+            return torch.empty(N, dtype=torch.int32, device=device)
+        return _out(labels, torch.int32, N, device, "labels")
+
+    def _scores(self, scores, want, N, device):
+        if scores is None:
+            return torch.empty(N, self.K, dtype=torch.float32, device=device) if want else None
+        return _out(scores, torch.float32, N * self.K, device, "scores")
+
     def recheck_count(self):
         return int(lib().hdc_model_recheck_count(self._h))
 
     def last_launch_count(self):
         return int(lib().hdc_model_last_launch_count(self._h))
+
+    def last_kernel(self):
+        """Kernel family of the last call: "none", "small", "ffma" or "tc" (hdc_model_last_kernel)."""
+        return KERNELS.get(int(lib().hdc_model_last_kernel(self._h)), "invalid")
 
     def set_kernel_timing(self, enable=True):
         _check(lib().hdc_model_set_kernel_timing(self._h, 1 if enable else 0))
@@ -208,6 +255,10 @@ class Model:
 def infer(X, B, C, prec="fp32", return_scores=False, stream=None):
     """One-shot hdc_infer(X, B, C, N, F, D, K) -> labels (+ scores)."""
     X, B, C = _dev_f32(X, "X"), _dev_f32(B, "B"), _dev_f32(C, "C")
+    if X.dim() != 2 or B.dim() != 2 or C.dim() != 2 or X.shape[1] != B.shape[0] or C.shape[1] != B.shape[1]:
+        raise ValueError("X (N x F), B (F x D), C (K x D) expected")
+    if not (X.device == B.device == C.device):
+        raise ValueError("X, B, C must be on one device")
     N, F = X.shape
     D = B.shape[1]
     K = C.shape[0]
@@ -227,9 +278,13 @@ def dshard_exchange_bytes(N, K, world):
 def argmax(S, labels=None, stream=None):
     """Lowest-index row argmax of S (N x K) -> int32 labels (hdc_argmax)."""
     S = _dev_f32(S, "S")
+    if S.dim() != 2:
+        raise ValueError("S must be N x K")
     N, K = S.shape
     if labels is None:
         labels = torch.empty(N, dtype=torch.int32, device=S.device)
+    else:
+        _out(labels, torch.int32, N, S.device, "labels")
     with torch.cuda.device(S.device):
         _check(lib().hdc_argmax(_ptr(S), N, K, _ptr(labels), _stream_ptr(stream, S.device)))
     return labels
@@ -242,15 +297,28 @@ def unpack_signs(H, D):
     return 1 - 2 * bits.to(torch.int8)
 
 
+def _packed(H, D):
+    if not (isinstance(H, torch.Tensor) and H.is_cuda and H.dtype == torch.int32 and H.dim() == 2
+            and H.is_contiguous() and H.shape[1] >= (D + 31) // 32):
+        raise TypeError("H must be a contiguous CUDA int32 tensor N x (>= ceil(D/32))")
+
+
 def similarity_packed(H, D, C, labels=None, scores=None, return_scores=True, stream=None):
     """Stage II + argmax over a packed H (the unfused ablation path)."""
     C = _dev_f32(C, "C")
+    _packed(H, D)
     N, ldw = H.shape
     K = C.shape[0]
+    if C.dim() != 2 or C.shape[1] != D:
+        raise ValueError("C must be K x D")
     if labels is None:
         labels = torch.empty(N, dtype=torch.int32, device=H.device)
+    else:
+        _out(labels, torch.int32, N, H.device, "labels")
     if scores is None and return_scores:
         scores = torch.empty(N, K, dtype=torch.float32, device=H.device)
+    elif scores is not None:
+        _out(scores, torch.float32, N * K, H.device, "scores")
     with torch.cuda.device(H.device):
         _check(lib().hdc_similarity_packed(_ptr(H), ldw, N, D, _ptr(C), K, _ptr(labels), _ptr(scores),
                                            _stream_ptr(stream, H.device)))
@@ -259,10 +327,15 @@ def similarity_packed(H, D, C, labels=None, scores=None, return_scores=True, str
 
 def bundle_classes(H, D, y, K, counts=None, return_M=True, stream=None):
     """Single-pass training: counts[k] += sum of h_n over class k; M = HardSign(counts)."""
+    _packed(H, D)
     N, ldw = H.shape
+    if not (isinstance(y, torch.Tensor) and y.device == H.device and y.numel() == N):
+        raise ValueError("y must hold N labels on H's device")
     y = y.to(torch.int32).contiguous()
     if counts is None:
         counts = torch.zeros(K, D, dtype=torch.int32, device=H.device)
+    else:
+        _out(counts, torch.int32, K * D, H.device, "counts")
     M = torch.empty(K, D, dtype=torch.float32, device=H.device) if return_M else None
     with torch.cuda.device(H.device):
         _check(lib().hdc_bundle_classes(_ptr(H), ldw, N, D, _ptr(y), K, _ptr(counts), _ptr(M),

@@ -78,3 +78,55 @@ def test_binding_fails_loudly_without_cuda_tensors():
     import paper_2506_09282_b200 as hdc
     with pytest.raises(TypeError):
         hdc.argmax(torch.zeros(3, 4))          # host tensor: no CPU fallback exists
+
+
+def test_binding_rejects_mismatched_outputs_before_the_c_call():
+    # the C layer writes N (N*K) elements through raw pointers: the binding must refuse
+    # outputs of the wrong dtype, size, layout or device instead of letting it overrun
+    import torch
+    from paper_2506_09282_b200.hdc import _out
+    cpu = torch.device("cpu")
+    ok = torch.empty(8, dtype=torch.int32)
+    assert _out(ok, torch.int32, 8, cpu, "labels") is ok
+    with pytest.raises(TypeError):
+        _out(torch.empty(8, dtype=torch.int64), torch.int32, 8, cpu, "labels")     # int64 labels
+    with pytest.raises(ValueError):
+        _out(torch.empty(7, dtype=torch.int32), torch.int32, 8, cpu, "labels")     # too short
+    with pytest.raises(ValueError):
+        _out(torch.empty(16, dtype=torch.int32)[::2], torch.int32, 8, cpu, "labels")  # strided
+    with pytest.raises(ValueError):
+        _out(ok, torch.int32, 8, torch.device("cuda", 0), "labels")               # wrong device
+    with pytest.raises(TypeError):
+        _out([0] * 8, torch.int32, 8, cpu, "labels")
+
+
+@pytest.mark.gpu
+def test_binding_rejects_wrong_widths_and_outputs_on_gpu(cuda_device):
+    import torch
+    import paper_2506_09282_b200 as hdc
+    B = torch.randn(20, 300, device=cuda_device)
+    C = torch.randn(4, 300, device=cuda_device)
+    m = hdc.Model(B, C, prec="fp32_tc")
+    X = torch.randn(10, 20, device=cuda_device)
+    with pytest.raises(ValueError):
+        m.infer(torch.randn(10, 19, device=cuda_device))
+    with pytest.raises(ValueError):
+        m.encode(torch.randn(10, 21, device=cuda_device))
+    with pytest.raises(ValueError):
+        m.partial_scores(torch.randn(10, 19, device=cuda_device))
+    with pytest.raises(ValueError):
+        m.infer(X, labels=torch.empty(9, dtype=torch.int32, device=cuda_device))
+    with pytest.raises(TypeError):
+        m.infer(X, labels=torch.empty(10, dtype=torch.int64, device=cuda_device))
+    with pytest.raises(ValueError):
+        m.infer(X, scores=torch.empty(10, 3, device=cuda_device))
+    with pytest.raises(ValueError):
+        m.infer_host(torch.randn(10, 19).pin_memory(), torch.empty(10, dtype=torch.int32).pin_memory())
+    with pytest.raises(TypeError):
+        m.infer_host(X.cpu().pin_memory(), torch.empty(10, dtype=torch.int64).pin_memory())
+    with pytest.raises(ValueError):
+        m.infer_host(X.cpu().pin_memory(), torch.empty(10, dtype=torch.int32, device=cuda_device))
+    y, _ = m.infer(X)
+    torch.cuda.synchronize()
+    assert y.shape == (10,)
+    m.close()

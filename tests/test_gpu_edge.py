@@ -6,8 +6,7 @@ import pytest
 import torch
 
 import oracle
-from oracle.policy import check_fp32, check_lowp
-from tests.gpu_util import run_model, to_dev
+from tests.gpu_util import check_result, run_model, to_dev
 
 pytestmark = pytest.mark.gpu
 PRECS = ["fp32", "fp32_tc", "tf32", "bf16"]
@@ -39,10 +38,8 @@ def test_empty_batch(hdc, prec):
     m.close()
 
 
-def _check(prec, orc, y, S, D):
-    if prec in ("fp32", "fp32_tc"):
-        return check_fp32(orc, y, S)
-    return check_lowp(orc, y, S, rtol=max(1e-2, 32.0 / D))
+def _check(prec, kernel, X, B, C, y, S):
+    return check_result(prec, kernel, X, B, C, y, S, north_star=False)
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -56,7 +53,7 @@ def test_tiny_dimensions(hdc, prec, N, F, D, K):
     m = hdc.Model(Bd, Cd, prec=prec)
     for path in ("small", "fused"):
         y, S = run_model(m, X, path)
-        rep = _check(prec, oracle.infer(X, B, C, allow=True), y, S, D)
+        rep = _check(prec, m.last_kernel(), X, B, C, y, S)
         if K == 1:
             assert np.all(y == 0)
         print(prec, path, (N, F, D, K), rep)
@@ -74,9 +71,10 @@ def test_all_zero_rows(hdc, prec):
     Bd, Cd = to_dev(B, C)
     m = hdc.Model(Bd, Cd, prec=prec)
     y, S = run_model(m, X, "auto")
+    kernel = m.last_kernel()
     m.close()
     rowsum = C.astype(np.float64).sum(axis=1)
     np.testing.assert_allclose(S[::7], np.broadcast_to(rowsum, S[::7].shape), rtol=1e-5,
                                atol=1e-4 * np.abs(C).sum(axis=1).max())
     assert np.all(y[::7] == int(np.argmax(rowsum)))
-    _check(prec, oracle.infer(X, B, C, allow=True), y, S, D)
+    _check(prec, kernel, X, B, C, y, S)
