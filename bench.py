@@ -5,11 +5,17 @@
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
     python bench.py --impl reference ...                    (the CPU oracle arm)
 
-A step = one hdc_model_infer call over one batch of the configuration (all of
-Alg. 1: encode, HardSign, similarity, argmax), inputs resident in HBM.  Multi-GPU
-runs are weak-scaling: every rank infers its own batch of the configuration
-(rows r*N..(r+1)*N of the generator stream); there is no data-path collective.
-Prints ONE JSON line (rank 0).
+A step = one pass of the hot path over one batch of the configuration (all of
+Alg. 1: encode, HardSign, similarity, argmax), inputs resident in HBM.  The
+default workload is BASELINE cfg5 (N=131072, F=3072, D=10000, K=10; the largest
+BASELINE config, quoted at 1/2/4/8 GPUs) in the sign-exact fp32_tc precision.
+
+Multi-GPU (one rank per GPU) strong-scales the config's batch, ScalableHD-L row
+ownership: rank r infers rows shard_bounds(N, world, r) and the step ends
+with the all-gather of every rank's int32 labels (the N-shard's only collective,
+inside the timed step).  --scaling weak instead gives every rank a whole batch (no
+collective); --dshard splits D (small N) with an all-reduce of the N x K partial
+scores or the in-kernel peer-memory exchange.  Prints ONE JSON line (rank 0).
 """
 import argparse
 import json
@@ -44,11 +50,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--prec", default="fp32_tc", choices=["fp32", "tf32", "bf16", "fp32_tc"])
     ap.add_argument("--path", default="auto", choices=["auto", "small", "fused"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's N split over the ranks + label all-gather "
+                         "in the step; weak: every rank infers a whole batch, no collective")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-peaks", action="store_true", help="skip the in-run cuBLAS peak probes")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--mode", default="infer", choices=["infer", "unfused", "train"],
                     help="infer: fused hot path (default); unfused: the fusion ablation "
@@ -198,7 +208,7 @@ def run_reference(args, rank, world):
     sample = "%d of %d rows of %s per step (rows are independent)" % (rows, cfg.N, cfg.name)
     out = {"impl": "reference", "metric": "samples_per_s", "value": value, "unit": "samples/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+           "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
                       "sample_rows": rows},
@@ -210,38 +220,89 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- ours
-def roofline_for(cfg, prec, path, ms_kernel, peaks, clock_mhz):
-    N, F, D, K = cfg.N, cfg.F, cfg.D, cfg.K
+def probe_peaks(dev):
+    """Dense tensor-core throughput measured in this run with cuBLAS (torch.matmul /
+    torch._int_mm, 8192^3, best of 10): the TF32 peak the tf32 path is judged against
+    (SURVEY §8d), plus bf16 and int8 as context next to MEASURED_PEAKS.json."""
+    import torch
+    out = {}
+    n = 8192
+    def best(fn, flop):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return flop / (min(ts) * 1e-3) / 1e12
+    try:
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        out["tf32_tflops"] = best(lambda: torch.matmul(a, b), 2.0 * n ** 3)
+        torch.backends.cuda.matmul.allow_tf32 = prev
+        a16, b16 = a.bfloat16(), b.bfloat16()
+        out["bf16_tflops"] = best(lambda: torch.matmul(a16, b16), 2.0 * n ** 3)
+        del a, b, a16, b16
+        ai = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=dev)
+        bi = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=dev).t()
+        out["int8_tops"] = best(lambda: torch._int_mm(ai, bi), 2.0 * n ** 3)
+        del ai, bi
+    except Exception as e:                              # a probe failing must not kill the bench
+        out["error"] = repr(e)[:200]
+    torch.cuda.empty_cache()
+    return out
+
+
+def roofline_for(cfg, prec, path, ms_kernel, peaks, run_peaks, units):
+    """Roofline object of the dominant kernel: algorithmic work per launch
+    / measured kernel time against the peak of the contraction's own dtype."""
+    N, F, D, K = units, cfg.F, cfg.D, cfg.K
     flops = 2.0 * N * F * D + 2.0 * N * D * K
     bytes_ = 4.0 * D * (F + K) + 4.0 * N * F + 4.0 * N
-    small = (path == "small") or (path == "auto" and N <= 32)
+    small = (path == "small") or (path == "auto" and N <= 32 and prec in ("fp32", "fp32_tc")) or \
+            (path == "auto" and N <= 8)
     if small:
         achieved = bytes_ / (ms_kernel * 1e-3) / 1e9
         peak = float(peaks["hbm_gbs"])
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
-                "algorithmic_per_launch": bytes_}
+                "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": bytes_,
+                "algorithmic_unit": "bytes: 4 D (F + K) + 4 N F + 4 N (B, C once; X; labels)"}
     achieved = flops / (ms_kernel * 1e-3) / 1e12
-    ceiling = None
+    bf16 = float(peaks["bf16_tflops"])
+    out = {"unit": "TFLOP/s", "traffic": None, "algorithmic_per_launch": flops,
+           "algorithmic_unit": "FLOP: 2 N F D + 2 N D K"}
     if prec == "fp32":
         mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak = N_SM * 128 * 2 * mhz * 1e6 / 1e12       # FFMA: 148 SM x 128 lanes x 2 flop
-        bound = "alu"
+        out.update(bound="alu", peak=peak, peak_basis="FFMA: 148 SM x 128 FMA/clk x 2 x sm_max_mhz")
+    elif prec == "fp32_tc":
+        # the contraction is tcgen05 kind::i8: int8 dense peak = measured bf16 x the guide's
+        # nominal 4.5 / 2.25 ratio; six int8 MMAs per algorithmic MAC (int8x3 limbs) cap
+        # this path at 1/6 of it (path_ceiling)
+        peak = 2.0 * bf16
+        out.update(bound="tensor", peak=peak,
+                   peak_basis="int8 = 2 x measured bf16 %.1f TFLOP/s (nominal 4.5/2.25 PF ratio)" % bf16,
+                   path_ceiling=peak / 6.0, frac_of_path_ceiling=achieved / (peak / 6.0),
+                   frac_of_bf16_peak=achieved / bf16)
+    elif prec == "tf32":
+        tf = run_peaks.get("tf32_tflops")
+        peak = float(tf) if tf else bf16 / 2.0
+        out.update(bound="tensor", peak=peak,
+                   peak_basis=("tf32 measured in this run (cuBLAS 8192^3)" if tf else
+                               "tf32 = measured bf16 / 2 (nominal ratio; in-run probe failed)"),
+                   frac_of_half_bf16=achieved / (bf16 / 2.0))
     else:
-        bf16 = float(peaks["bf16_tflops"])
-        peak = bf16 / 2.0 if prec == "tf32" else bf16  # tf32 dense = 1/2 bf16 (nominal ratio)
-        bound = "tensor"
-        if prec == "fp32_tc":
-            # sign-exact int8 limbs: 6 int8 MMAs per MAC = 3 bf16-MMA equivalents
-            ceiling = bf16 / 3.0
-    out = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-           "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": flops}
-    if ceiling:
-        out["path_ceiling"] = ceiling
-        out["frac_of_path_ceiling"] = achieved / ceiling
-    if bound == "tensor":
-        # what the fused tcgen05 kernel spends beyond the MMA floor
-        out["limit"] = "MMA floor per K stage + ~2000 cycles per tile (epilogue/Stage II/TMA interference), DESIGN.md §11"
+        out.update(bound="tensor", peak=bf16, peak_basis="bf16 measured (MEASURED_PEAKS.json, burst)",
+                   frac_of_sustained=achieved / float(peaks.get("bf16_tflops_sustained", bf16)))
+    out["achieved"] = achieved
+    out["frac"] = achieved / out["peak"]
     return out
 
 
@@ -251,30 +312,41 @@ def run_ours(args, rank, world, local_rank):
     from hdc_inputs import CONFIGS, make_B, make_C
     from hdc_inputs.device import make_X_device
     import paper_2506_09282_b200 as hdc
+    from paper_2506_09282_b200.sharding import shard_bounds
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg = CONFIGS[args.config]
     peaks, peaks_src = load_peaks()
     Bh, Ch = make_B(cfg), make_C(cfg)
+    strong = args.scaling == "strong" and not args.dshard
     if args.dshard:
         # D-shard: this rank's column slice of B and C; X replicated (rows 0..N)
         from paper_2506_09282_b200.sharding import d_shard_slices
         dlo, dhi = d_shard_slices(cfg.D, world)[rank]
         Bh, Ch = Bh[:, dlo:dhi].copy(), Ch[:, dlo:dhi].copy()
-        X = make_X_device(cfg, dev, 0, cfg.N)
+        r0, r1 = 0, cfg.N
+    elif strong:
+        # N-shard (ScalableHD-L row ownership): this rank's rows of the batch
+        r0, r1 = shard_bounds(cfg.N, world, rank)
     else:
         # weak scaling: rank r infers rows [r N, (r+1) N) of the X stream
-        X = make_X_device(cfg, dev, rank * cfg.N, (rank + 1) * cfg.N)
+        r0, r1 = rank * cfg.N, (rank + 1) * cfg.N
+    n_local = r1 - r0
+    X = make_X_device(cfg, dev, r0, r1)
     B = torch.from_numpy(Bh).to(dev)
     C = torch.from_numpy(Ch).to(dev)
     model = hdc.Model(B, C, prec=args.prec)
-    labels = torch.empty(cfg.N, dtype=torch.int32, device=dev)
+    counts = [hi - lo for lo, hi in (shard_bounds(cfg.N, world, r) for r in range(world))]
+    n_pad = max(counts) if strong else n_local
+    lab_pad = torch.zeros(n_pad, dtype=torch.int32, device=dev)      # this rank's labels
+    labels = lab_pad[:n_local]
+    lab_all = torch.empty(n_pad * world, dtype=torch.int32, device=dev) if (strong and world > 1) else None
     stream = torch.cuda.current_stream(dev)
     Sbuf = torch.empty(cfg.N, cfg.K, dtype=torch.float32, device=dev)
-    Hbuf = torch.empty(cfg.N, (cfg.D + 31) // 32, dtype=torch.int32, device=dev)
-    ytrain = (torch.arange(cfg.N, device=dev, dtype=torch.int32) * 7919) % cfg.K
-    counts = torch.zeros(cfg.K, cfg.D, dtype=torch.int32, device=dev)
+    Hbuf = torch.empty(n_local, (cfg.D + 31) // 32, dtype=torch.int32, device=dev)
+    ytrain = (torch.arange(n_local, device=dev, dtype=torch.int32) * 7919) % cfg.K
+    counts_tr = torch.zeros(cfg.K, cfg.D, dtype=torch.int32, device=dev)
     xchg = None
     if args.dshard and args.dshard_exchange == "kernel" and cfg.N <= 32:
         from paper_2506_09282_b200.sharding import DShardExchange
@@ -290,8 +362,8 @@ def run_ours(args, rank, world, local_rank):
             hdc.similarity_packed(Hbuf, cfg.D, C, labels=labels, return_scores=False)
         elif args.mode == "train":
             model.encode(X, H=Hbuf)
-            counts.zero_()
-            hdc.bundle_classes(Hbuf, cfg.D, ytrain, cfg.K, counts=counts, return_M=False)
+            counts_tr.zero_()
+            hdc.bundle_classes(Hbuf, cfg.D, ytrain, cfg.K, counts=counts_tr, return_M=False)
         elif xchg is not None:
             xchg.infer(model, X)
         elif args.dshard:
@@ -301,14 +373,27 @@ def run_ours(args, rank, world, local_rank):
             hdc.argmax(Sbuf, labels=labels)
         else:
             model.infer(X, labels=labels, path=args.path)
+            if lab_all is not None:                  # N-shard: gather every rank's labels
+                dist.all_gather_into_tensor(lab_all, lab_pad)
+
+    run_peaks = {} if args.no_peaks else probe_peaks(dev)
+    # L2 flush between timed steps (untimed): write a 2x L2 buffer, then READ another one,
+    # so the timed step starts with L2 full of clean lines of unrelated data (no dirty
+    # write-backs of the flush competing with the step's own reads)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+    flush_w = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+    flush_r = torch.ones(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+    sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def flush(i):
+        flush_w.fill_(float(i))
+        torch.sum(flush_r, dim=0, out=sink)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches_per_step = model.last_launch_count() + (1 if args.dshard and xchg is None else 0) + \
-        {"infer": 0, "unfused": 2, "train": 4}[args.mode]   # + memset/similarity, memset/sort/bundle
+        {"infer": 0, "unfused": 2, "train": 4}[args.mode]   # + argmax / similarity, memset/sort/bundle
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -318,7 +403,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks.start()
     for i in range(args.steps):
-        flush.fill_(float(i))                          # evict X, B, C from L2 (untimed)
+        flush(i)
         starts[i].record(stream)
         step()
         ends[i].record(stream)
@@ -333,7 +418,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    units = cfg.N if args.dshard else cfg.N * world
+    units = cfg.N if (args.dshard or strong) else cfg.N * world
     value = units * args.steps / (total_ms * 1e-3)
 
     # dominant-kernel duration (library-recorded CUDA events on the launching
@@ -341,17 +426,48 @@ def run_ours(args, rank, world, local_rank):
     model.set_kernel_timing(True)
     kms = []
     for i in range(args.steps):
-        flush.fill_(float(i))
+        flush(i)
         step()
         kms.append(model.last_kernel_ms())
     model.set_kernel_timing(False)
     kernel_ms = sum(kms) / len(kms)
+    kernel = model.last_kernel()
+
+    # small batches: the warm figure -- a CUDA graph of 200 back-to-back
+    # calls (no flush, B and C may stay in L2), time / 200
+    warm = None
+    if n_local <= 32 and world == 1 and args.mode == "infer" and not args.dshard:
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                step()                               # warm on the capture stream
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=side):
+                    for _ in range(200):
+                        step()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            wms = a.elapsed_time(b) / 200
+            warm = {"us_per_call": wms * 1e3, "value": n_local / (wms * 1e-3), "unit": "samples/s",
+                    "hbm_frac_if_streamed": (4.0 * cfg.D * (cfg.F + cfg.K) / (wms * 1e-3) / 1e9) /
+                    float(peaks["hbm_gbs"]),
+                    "how": "CUDA graph of 200 back-to-back calls / 200, no L2 flush (B, C may be L2-resident)"}
+        except Exception as e:
+            warm = {"error": repr(e)[:200]}
 
     # end to end through the public host-buffer entry point (H2D X, D2H labels)
     e2e = None
     if not args.no_e2e and not args.dshard and args.mode == "infer":
         Xh = X.cpu().pin_memory()
-        yh = torch.empty(cfg.N, dtype=torch.int32).pin_memory()
+        yh = torch.empty(n_local, dtype=torch.int32).pin_memory()
         # warm the host path to steady state: the first tens of back-to-back calls run up
         # to 3x slower while the host-device link ramps up (measured: 2.1 -> 0.74 ms per
         # cfg2 call over ~20 calls), so warm up for >= 30 calls and >= 0.2 s
@@ -375,36 +491,63 @@ def run_ours(args, rank, world, local_rank):
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": cfg.N * world * args.steps / (float(te.item()) * 1e-3), "unit": "samples/s",
-               "h2d_bytes_per_step": int(Xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4)}
+        e2e = {"value": units * args.steps / (float(te.item()) * 1e-3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4) * (world if strong else 1),
+               "d2h_bytes_per_step": int(yh.numel() * 4) * (world if strong else 1),
+               "api": "hdc_model_infer_host (pinned host X -> labels in mapped pinned host memory)",
+               "gather": "none: each rank's labels land in its own host memory" if world > 1 else None}
+
+    # one-shot hdc_infer (model creation inside the call), reported separately
+    one_shot = None
+    if world == 1 and args.mode == "infer" and not args.dshard:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hdc.infer(X, B, C, prec=args.prec)
+        torch.cuda.synchronize()
+        one_shot = {"ms": 1e3 * (time.perf_counter() - t0),
+                    "how": "wall clock of one hdc_infer(X, B, C) call incl. model creation "
+                           "(B, C layout copies), synchronised"}
 
     if rank != 0:
         return
-    roof = roofline_for(cfg, args.prec, args.path, kernel_ms, peaks, clk["sm_mhz"])
+    path = args.path
+    if path == "auto":
+        path = "small" if kernel == "small" else "fused"
+    roof = roofline_for(cfg, args.prec, path, kernel_ms, peaks, run_peaks, n_local)
     roof["peak_source"] = peaks_src
     roof["traffic"] = measured_traffic(cfg.name, args.prec)
     if roof["traffic"] is not None:
         roof["traffic_source"] = "ncu --set full dram bytes per launch (profiles/**/traffic.json)"
+    roof["kernel"] = kernel
     roof["kernel_ms"] = kernel_ms
     roof["kernel_share_of_step"] = kernel_ms / ms_per_step
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         rate, rows, dt, threads, _ = oracle_rate(cfg, args.cpu_seconds)
+        rate1, rows1, dt1, _, _ = oracle_rate(cfg, min(6.0, args.cpu_seconds / 2), nthreads=1)
         cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",
                "sample": "first %d of %d rows of %s (%.1f s, rows independent)" % (rows, cfg.N, cfg.name, dt),
+               "single_thread": {"value": rate1, "unit": "samples/s/core", "cores": 1,
+                                 "sample": "first %d rows (%.1f s)" % (rows1, dt1)},
                "cpu": cpu_model()}
     out = {"metric": "samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-           "higher_is_better": True, "scaling": "strong" if args.dshard else "weak", "vs_baseline": None,
+           "higher_is_better": True,
+           "scaling": "strong" if (args.dshard or strong) else "weak", "vs_baseline": None,
            "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16", "fp32_tc": "i8x3"}[args.prec],
            "data": "synthetic",
            "config": {"workload": cfg.name, "N": cfg.N, "F": cfg.F, "D": cfg.D, "K": cfg.K,
                       "prec": args.prec, "path": args.path, "mode": args.mode, "global_batch": units,
-                      "parallelism": ("dshard%d" % world) if args.dshard else ("dp%d" % world),
+                      "rows_per_rank": n_local,
+                      "parallelism": ("dshard%d" % world) if args.dshard else ("nshard%d" % world if strong else "dp%d" % world),
+                      "collective": ("all_gather_into_tensor(int32 labels) in the step" if (strong and world > 1) else
+                                     ("all_reduce(N x K scores)" if (args.dshard and xchg is None and world > 1) else
+                                      ("in-kernel peer-memory exchange" if xchg is not None else None))),
                       "dshard_exchange": (("kernel" if xchg is not None else "nccl") if args.dshard else None),
-                      "l2": "flushed between steps (write of 2x L2 bytes, untimed)",
+                      "l2": "flushed between steps (untimed write of 2x L2 bytes, then a read of another 2x L2 buffer)",
                       "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
-           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "warm": warm, "one_shot": one_shot,
+           "peaks_in_run": run_peaks,
            "gpu_launches": launches_per_step * args.steps, "clocks": clk,
            "ms_per_step_min": min(ms), "ms_per_step_median": sorted(ms)[len(ms) // 2]}
     print(json.dumps(out), flush=True)
@@ -421,6 +564,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")         # communicator lines show the rank count
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
