@@ -512,7 +512,7 @@ def run_ours(args, rank, world, local_rank):
         return
     path = args.path
     if path == "auto":
-        path = "small" if kernel == "small" else "fused"
+        path = "small" if kernel in ("small", "small_tc") else "fused"
     roof = roofline_for(cfg, args.prec, path, kernel_ms, peaks, run_peaks, n_local)
     roof["peak_source"] = peaks_src
     roof["traffic"] = measured_traffic(cfg.name, args.prec)

@@ -205,10 +205,18 @@ int32_t hdc_model_last_launch_count(hdc_model_t m);
 
 /* Kernel family that computed the last call on this model (diagnostic; -1 on a NULL
  * model).  The arithmetic differs by family, which is what the parity tests key on:
- *   HDC_KERNEL_SMALL: fp32 streaming D-split kernel (sign-exact, any precision's model);
- *   HDC_KERNEL_FFMA:  fp32 fused FFMA kernel (sign-exact);
- *   HDC_KERNEL_TC:    fused tcgen05 kernel in the model's precision. */
-typedef enum { HDC_KERNEL_NONE = 0, HDC_KERNEL_SMALL = 1, HDC_KERNEL_FFMA = 2, HDC_KERNEL_TC = 3 } hdc_kernel_t;
+ *   HDC_KERNEL_SMALL:    fp32 streaming D-split kernel (sign-exact, any precision's model);
+ *   HDC_KERNEL_FFMA:     fp32 fused FFMA kernel (sign-exact);
+ *   HDC_KERNEL_TC:       fused tcgen05 kernel in the model's precision;
+ *   HDC_KERNEL_SMALL_TC: int8 tensor-core streaming D-split kernel (HDC_PREC_FP32_TC models,
+ *                        N <= 32; sign-exact). */
+typedef enum {
+  HDC_KERNEL_NONE = 0,
+  HDC_KERNEL_SMALL = 1,
+  HDC_KERNEL_FFMA = 2,
+  HDC_KERNEL_TC = 3,
+  HDC_KERNEL_SMALL_TC = 4
+} hdc_kernel_t;
 int32_t hdc_model_last_kernel(hdc_model_t m);
 
 /* Diagnostics for roofline reporting: when enabled, each call records CUDA

@@ -41,6 +41,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 constexpr int64_t kMaxF = int64_t(1) << 20;
 constexpr int kSmallMaxN = 32;
 constexpr int kSmallMaxNLowp = 8;          // bf16 / tf32 models (see run())
+constexpr int kSmallTcMinN = 5;            // fp32_tc models: K2t from this many rows (see run())
 constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 
 }  // namespace
@@ -81,6 +82,9 @@ struct hdc_model_s {
   float* Cp = nullptr;
   float* bnorm = nullptr;
   // small-batch workspace
+  unsigned long long* acc_t = nullptr;   // K2t: [32][K] int64 fixed-point score accumulators
+  unsigned* cnt_t = nullptr;             // K2t: [1] arrival counter
+  uint8_t* ximg_t = nullptr;             // K2t: X limb image
   float* S_part = nullptr;
   unsigned* cnt = nullptr;  // [4] last-arriver counter of K2
   unsigned long long* recheck = nullptr;
@@ -172,6 +176,9 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Cp);
   cudaFree(m->bnorm);
   cudaFree(m->S_part);
+  cudaFree(m->acc_t);
+  cudaFree(m->cnt_t);
+  cudaFree(m->ximg_t);
   cudaFree(m->cnt);
   cudaFree(m->recheck);
   cudaFree(m->Xdev);
@@ -393,6 +400,38 @@ hdc_status_t run(hdc_model_s* m, const float* X, int64_t N, int32_t* labels, flo
     path = (N <= small_max) ? HDC_PATH_SMALL : HDC_PATH_FUSED;
   }
   if (path == HDC_PATH_FUSED) return run_fused(m, X, N, labels, scores, recheck, st);
+  // sign-exact models: the int8 tensor-core small-batch kernel (B streamed as 3-byte limbs,
+  // Stage I on the tensor cores) from kSmallTcMinN rows; below it the fp32 streaming kernel,
+  // whose single launch beats K2t's two (cfg3: N = 1 18.8 vs 19.8 us, N = 4 20.1 vs 21.6 us;
+  // N = 16 28.9 vs 21.9 us, N = 32 43.2 vs 23.9 us).  HDC_SMALL_TC=0/1 forces either.
+  const char* stc = getenv("HDC_SMALL_TC");
+  const bool want_tc = stc ? (atoi(stc) != 0) : (N >= kSmallTcMinN);
+  if (m->acc_t && tc_eligible(m) && N <= kSmallMaxN && want_tc && !getenv("HDC_SMALL_FP32") &&
+      small_tc_fits(m->F, m->D, m->K, (int)N, m->num_sms)) {
+    SmallTcOperands o;
+    o.F = m->F;
+    o.Fp = m->Fp;
+    o.D = m->D;
+    o.Dp = m->Dp;
+    o.Dq = m->Dq;
+    o.K = m->K;
+    o.Btc = (const int8_t*)m->Btc;
+    o.coltau = m->coltau;
+    o.Bt = m->Bt;
+    o.Cp = m->Cp;
+    o.shift = m->corr_shift;
+    o.acc = m->acc_t;
+    o.cnt = m->cnt_t;
+    o.recheck = m->recheck;
+    o.ximg = m->ximg_t;
+    m->tic(st);
+    cudaError_t e = launch_small_tc(o, X, (int)N, scores, labels, m->num_sms, st);
+    m->toc(st);
+    if (e != cudaSuccess) return cuda_fail(e, "small tensor-core launch");
+    m->last_launches = 2;
+    m->last_kernel = HDC_KERNEL_SMALL_TC;
+    return HDC_OK;
+  }
   const SmallWorkspace ws = m->small_ws();
   const int chunk = small_max_rows(m->F, m->D, m->K, m->num_sms);
   if (chunk < 1) return fail(HDC_ERR_UNSUPPORTED, "F too large for the small-batch kernel's shared memory");
@@ -513,6 +552,12 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
     if (e == cudaSuccess && mode == 2) {
       e = cudaDeviceSynchronize();
       if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
+      // K2t (small-batch tensor-core kernel) accumulators, zero between launches
+      if (e == cudaSuccess) e = cudaMalloc((void**)&m->acc_t, sizeof(unsigned long long) * kSmallMaxN * K);
+      if (e == cudaSuccess) e = cudaMemset(m->acc_t, 0, sizeof(unsigned long long) * kSmallMaxN * K);
+      if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_t, sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMemset(m->cnt_t, 0, sizeof(unsigned));
+      if (e == cudaSuccess) e = cudaMalloc((void**)&m->ximg_t, (size_t)small_tc_image_bytes(F));
     }
   }
   if (e == cudaSuccess) e = cudaMemset(m->recheck, 0, sizeof(unsigned long long));

@@ -46,6 +46,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tc_limbs.cuh"
 
 namespace hdc {
 namespace {
@@ -234,27 +235,6 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// float64 re-evaluation of V[row, d] (fixed lane order, warp-cooperative).
-__device__ __forceinline__ float recheck_dot(const float* __restrict__ xr, const float* __restrict__ br,
-                                             int64_t F, int lane) {
-  // lane sums f = lane, lane + 32, ... in f order (fixed), then a fixed butterfly; 32
-  // independent loads in flight per chunk of 512 elements (one memory round trip each)
-  constexpr int U = 16;
-  double s = 0.0;
-  for (int64_t f0 = 0; f0 < F; f0 += 32 * U) {
-    float xv[U], bv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t f = f0 + 32 * u + lane;
-      xv[u] = f < F ? __ldg(xr + f) : 0.f;
-      bv[u] = f < F ? __ldg(br + f) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) s = fma((double)xv[u], (double)bv[u], s);   // 0 x 0 adds exactly 0
-  }
-  s = warp_sum_xor(s);
-  return s >= 0.0 ? 1.f : -1.f;
-}
 __device__ __forceinline__ float recheck_warp(const TcParams& p, int64_t row, int64_t d, int lane) {
   return recheck_dot(p.X + row * p.F, p.Bt + d * p.Fp, p.F, lane);
 }
@@ -972,40 +952,6 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // ---------------------------------------------------------------- operand prep
-// Balanced base-128 digits of the 21-bit integer image U = rint(x * c).
-__device__ __forceinline__ void limbs_of(float x, float c, int& d0, int& d1, int& d2, int& U) {
-  int u = __float2int_rn(x * c);
-  u = max(-2080768, min(2080768, u));
-  d2 = ((u + 64) & 127) - 64;
-  const int u1 = (u - d2) >> 7;
-  d1 = ((u1 + 64) & 127) - 64;
-  d0 = (u1 - d1) >> 7;
-  U = u;
-}
-
-__device__ __forceinline__ float scale_for(float amax) {
-  if (!(amax > 0.f)) return 1.f;
-  double c = 2080768.0 / (double)amax;
-  if (c > 1e37) c = 1e37;
-  return (float)c * (1.f - 9.5367431640625e-07f);  // (1 - 2^-20): keeps |x c| < 127*2^14
-}
-
-// Four consecutive elements f0..f0+3 of a source row (zero past F and for padding rows);
-// one 16-byte load when the row start and f0 are 16-byte aligned and all four are < F.
-__device__ __forceinline__ void load4(const float* __restrict__ row, int64_t f0, int64_t F, bool valid,
-                                      bool vec, float* x) {
-  if (valid && vec && f0 + 3 < F) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(row + f0));
-    x[0] = v.x;
-    x[1] = v.y;
-    x[2] = v.z;
-    x[3] = v.w;
-  } else {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) x[e] = (valid && f0 + e < F) ? __ldg(row + f0 + e) : 0.f;
-  }
-}
-
 // int8 limbs of four elements -> one 4-byte store per limb; returns their L1(U).
 __device__ __forceinline__ long long emit_limbs4(const float* x, float c, int8_t* __restrict__ out,
                                                  int64_t rows_p, int64_t r, int64_t Fp, int64_t f0) {
@@ -1024,15 +970,6 @@ __device__ __forceinline__ long long emit_limbs4(const float* x, float c, int8_t
   *reinterpret_cast<uint32_t*>(out + (1 * rows_p + r) * Fp + f0) = w1;
   *reinterpret_cast<uint32_t*>(out + (2 * rows_p + r) * Fp + f0) = w2;
   return l1;
-}
-
-// tau of a row from its L1(U): |c_x c_b x.b - U_x.U_b| <= 0.625 (L1(U_x) + L1(U_b)) +
-// 0.3907 F and the dropped limb products (i + j >= 3) add <= F (2^20 + 2^12) (DESIGN.md
-// §4).  The kernel compares I = A0 2^14 + A1 2^7 + A2 = (U_x.U_b - dropped) / 2^14, so
-// tau is stored / 2^14, rounded up: ceil((5 l1 / 8 + tau_const) / 2^14)
-// = (5 l1 + 8 tau_const + 2^17 - 1) >> 17.
-__device__ __forceinline__ int64_t row_tau(long long l1, int64_t tau_const, bool valid) {
-  return valid ? ((5 * l1 + 8 * tau_const + 131071) >> 17) + 1 : -(int64_t(1) << 62);
 }
 
 // One warp per row of a row-major [rows][F] fp32 matrix (X rows, or B^T rows): int8
@@ -1385,6 +1322,14 @@ cudaError_t launch_cluster(int cl_n, int cl_d, int virt, const CUtensorMap& a, c
 }
 
 }  // namespace
+
+bool make_tensor_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                        uint32_t box_outer, int swizzle_bytes) {
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return make_map_2d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, base, inner, outer, box_inner, box_outer, sw);
+}
 
 int tc_tile_n(int mode, int64_t K) { return tile_n_for(mode, K); }
 int64_t tc_s_part_slots(int64_t Tn, int64_t Td, int cl_n, int cl_d, int virt, int num_sms) {

@@ -2,6 +2,7 @@
 // kernels.  Not installed; the public boundary is include/hdc.h.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace hdc {
@@ -121,6 +122,31 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
 cudaError_t launch_tc_recheck(const TcOperands& o, int64_t N, float* S, int32_t* labels, int shift,
                               cudaStream_t st);
 int tc_corr_shift(const float* Cp, int64_t n, int64_t D);   // fixed-point shift for |C| (synchronous)
+// 2-D uint8 tensor map (row-major [outer][inner] bytes) with the given box and swizzle.
+bool make_tensor_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                        uint32_t box_outer, int swizzle_bytes);
+
+// K2t (k_small_tc.cu): small-batch (n <= 32) sign-exact inference on the int8 tensor cores
+// for HDC_PREC_FP32_TC models: each CTA streams the int8 limbs of its D-range of B^T once,
+// X's limbs are built in shared memory by every CTA, HardSign + float64 rechecks + Stage II
+// in the CTA, partial scores summed exactly in int64 fixed point (2^-shift units) by
+// atomics, the last CTA converts and takes the argmax.
+struct SmallTcOperands {
+  int64_t F, Fp, D, Dp, Dq, K;
+  const int8_t* Btc;                 // [3][Dq][Fp] limbs of B^T
+  const int64_t* coltau;             // [Dq]
+  const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
+  const float* Cp;                   // [K][Dp]
+  int shift;                         // fixed-point shift (tc_corr_shift)
+  unsigned long long* acc;           // [32 K] int64 accumulators, zero between launches
+  unsigned* cnt;                     // [1], zero between launches
+  unsigned long long* recheck;
+  uint8_t* ximg;                     // [small_tc_image_bytes(F)] X limb image workspace
+};
+int64_t small_tc_image_bytes(int64_t F);
+bool small_tc_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms);
+cudaError_t launch_small_tc(const SmallTcOperands& o, const float* X, int n, float* scores, int32_t* labels,
+                            int num_sms, cudaStream_t st);
 
 // k_packed.cu: unfused Stage II from bit-packed H (ablation) and class bundling (training)
 cudaError_t launch_packed_similarity(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,

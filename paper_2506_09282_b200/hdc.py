@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("HDC_LIB_PATH") or os.path.join(
 
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2, "fp32_tc": 3}
 PATH = {"auto": 0, "small": 1, "fused": 2}
-KERNELS = {0: "none", 1: "small", 2: "ffma", 3: "tc"}
+KERNELS = {0: "none", 1: "small", 2: "ffma", 3: "tc", 4: "small_tc"}
 _STATUS = {0: "HDC_OK", 1: "HDC_ERR_INVALID_VALUE", 2: "HDC_ERR_MISALIGNED",
            3: "HDC_ERR_UNSUPPORTED", 4: "HDC_ERR_NO_MEMORY", 5: "HDC_ERR_CUDA"}
 

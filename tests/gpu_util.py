@@ -29,7 +29,7 @@ def check_result(prec, kernel, X, B, C, y, S, north_star=True):
     if prec in LOWP and kernel == "tc":
         exact, rounded = oracle.infer_lowp(X, B, C, prec, nthreads=0)
         return check_lowp(exact, y, S, rtol=1e-2 if north_star else None, rounded=rounded)
-    assert kernel in ("small", "ffma", "tc", "none"), kernel
+    assert kernel in ("small", "small_tc", "ffma", "tc", "none"), kernel
     orc = oracle.infer(X, B, C, allow=True, nthreads=0)
     return check_fp32(orc, y, S)
 

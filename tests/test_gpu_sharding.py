@@ -69,31 +69,33 @@ def _slot(buf, world, stride, parity, sender):
     return buf[off:off + stride]
 
 
-@pytest.mark.parametrize("N", [1, 13, 32])
-def test_dshard_exchange_two_ranks_simulated(cuda_device, N):
+@pytest.mark.parametrize("Ns", [(1, 1, 1), (13, 13, 13), (32, 32, 32), (32, 5, 17, 1, 32)])
+def test_dshard_exchange_two_ranks_simulated(cuda_device, Ns):
     # Rank 0 of a 2-rank exchange on one GPU, WITHOUT a second kernel: rank 1's partial and
     # its signal are placed in rank 0's buffer beforehand, so the kernel never waits on
     # another kernel.  Checks the rank-order sum, the stores into the peer buffer and the
-    # signals, for both parities.
+    # signals, for both parities -- and with N changing from call to call on the same
+    # buffers (slots are sized for 32 rows, so their offsets never depend on N).
     import paper_2506_09282_b200 as hdc
     cfg = CONFIGS["cfg3_n32"]
-    X, B, C = make_X(cfg, 0, N), make_B(cfg), make_C(cfg)
+    X, B, C = make_X(cfg, 0, 32), make_B(cfg), make_C(cfg)
     Xd, Bd, Cd = to_dev(X, B, C)
     cut = 4996                                        # multiple of 4 (d_shard_slices alignment)
     ma = hdc.Model(Bd[:, :cut].contiguous(), Cd[:, :cut].contiguous(), prec="fp32")
     mb = hdc.Model(Bd[:, cut:].contiguous(), Cd[:, cut:].contiguous(), prec="fp32")
     W, K = 2, cfg.K
-    nwords = hdc.dshard_exchange_bytes(N, K, W) // 4
-    stride = (N * K + 3) // 4 * 4
+    nwords = hdc.dshard_exchange_bytes(32, K, W) // 4
+    assert all(hdc.dshard_exchange_bytes(n, K, W) // 4 == nwords for n in (1, 7, 32))
+    stride = (32 * K + 3) // 4 * 4                    # slot floats: N-independent
     bufs = [torch.zeros(nwords, dtype=torch.float32, device="cuda") for _ in range(W)]
     ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
-    Sa = ma.partial_scores(Xd)
-    Sb = mb.partial_scores(Xd)
-    for epoch in (1, 2, 3):
+    for epoch, N in enumerate(Ns, start=1):
         par = epoch & 1
+        Sa = ma.partial_scores(Xd[:N])
+        Sb = mb.partial_scores(Xd[:N])
         _slot(bufs[0], W, stride, par, 1)[:N * K] = Sb.reshape(-1)            # rank 1's partial
         bufs[0][:W].view(torch.int32)[1] = epoch                              # ... and its signal
-        y, S = ma.infer_dshard(Xd, ptrs, 0, W, epoch, return_scores=True)
+        y, S = ma.infer_dshard(Xd[:N], ptrs, 0, W, epoch, return_scores=True)
         torch.cuda.synchronize()
         expect = Sa + Sb                                                      # rank order
         assert torch.equal(S, expect)
