@@ -77,7 +77,7 @@ struct hdc_model_s {
   int64_t hout_ldw = 0;
   void* Atc = nullptr;       // [NL][Np][Fp]
   int64_t* rowtau = nullptr; // [Np]
-  float* S_part_tc = nullptr;
+  long long* S_part_tc = nullptr;
   unsigned* cnt_tc = nullptr;
   float* Cp = nullptr;
   float* bnorm = nullptr;
@@ -259,7 +259,7 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   m->tw_slots = 0;
   cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * rows * m->Fp);
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(int64_t) * rows);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(float) * nsl * kTileM * m->K);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(long long) * nsl * kTileM * tc_kp(m->K));
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess && mode == 2) {
@@ -330,6 +330,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.coltau = m->coltau;
   o.S_part = m->S_part_tc;
   o.s_part_slots = m->tw_slots;
+  o.shift = m->corr_shift;
   o.cnt = m->cnt_tc;
   o.recheck = m->recheck;
   o.Cp = m->Cp;
@@ -549,9 +550,11 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
     if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Dq, m->Cil, st0);
+    // fixed point of the exact Stage II sums (all tensor-core modes) and of the int8 mode's
+    // recheck corrections
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
     if (e == cudaSuccess && mode == 2) {
-      e = cudaDeviceSynchronize();
-      if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
       // K2t (small-batch tensor-core kernel) accumulators, zero between launches
       if (e == cudaSuccess) e = cudaMalloc((void**)&m->acc_t, sizeof(unsigned long long) * kSmallMaxN * K);
       if (e == cudaSuccess) e = cudaMemset(m->acc_t, 0, sizeof(unsigned long long) * kSmallMaxN * K);

@@ -74,6 +74,7 @@ constexpr int EPI_WARP0 = 4;
 constexpr int NUM_CQ = NUM_EPI / 4;                 // column groups of the tile
 constexpr int MAX_LIMBS = 3;
 constexpr int CORE_LBO = 128;                        // K-adjacent 8x16B core matrices
+constexpr int XCHG_BYTES = 128 * 8;                  // per-row (best value, index) of column group 1
 constexpr int KP_MAX_I8 = 32;                        // Stage II N (classes) limits
 constexpr int KP_MAX_16 = 64;
 
@@ -122,14 +123,15 @@ struct Cfg {
   static constexpr int H_REGION = H_TMEM ? 0 : NH * H_BYTES;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
-  static constexpr int FIXED = H_REGION + 2 * C_SLOT + 512 + 1024 + 16;
+  static constexpr int FIXED = H_REGION + 2 * C_SLOT + 512 + 1024 + 16 + XCHG_BYTES;
   static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / (A_STAGE + B_STAGE);
   static constexpr int STAGES_ = STAGES_FIT < STAGES_MAX ? STAGES_FIT : STAGES_MAX;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES_ * A_STAGE;
   static constexpr int OFF_H = OFF_B + STAGES_ * B_STAGE;
   static constexpr int OFF_C = OFF_H + H_REGION;
-  static constexpr int OFF_BAR = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;
+  static constexpr int OFF_X = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;   // argmax exchange [BM] x (value, index)
+  static constexpr int OFF_BAR = OFF_X + XCHG_BYTES;
   static constexpr int TOTAL = OFF_BAR + 512;
   static_assert(STAGES_ >= ((KBYTES == 128 && MODE == 2) || NAT > 1 ? 2 : 3), "pipeline depth");
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
@@ -148,7 +150,9 @@ struct TcParams {
   const int64_t* coltau;   // int8 mode: per-column part of tau
   const uint8_t* Cil;      // per D-tile Stage II operand (see Cfg::C_SLOT), c_tile_bytes each
   uint32_t c_tile_bytes;
-  float* S_part;           // [CTAs][nslot][BM][K] partial scores of split N-tiles
+  long long* S_part;       // [CTAs][nslot][BM][Kp] int64 fixed-point partial scores of split N-tiles
+  double scale, inv_scale; // 2^shift, 2^-shift: the fixed point of the Stage II sums (tc_corr_shift)
+  float scale_f;           // 2^shift as a normal float, else 0 (then the fp64 conversion)
   int64_t s_part_cap;      // capacity of S_part in [BM][K] slots
   int nslot;               // slots per CTA: 2 (CLD = 1: first / last N-group of the range),
                            // else one per N-group of the cluster's range
@@ -286,8 +290,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint64_t* cempty = cfull + 2;          // [2] C tile consumed (Stage II MMA done)
   uint64_t* hfull = cempty + 2;          // [NH] H tile written
   uint64_t* hempty = hfull + 2;          // [NH] H tile consumed
-  uint64_t* sfull = hempty + 2;          // [1] Stage II accumulator of a run complete
-  uint64_t* sempty = sfull + 1;          // [1] Stage II accumulator drained
+  uint64_t* sfull = hempty + 2;          // [1] Stage II accumulator of a tile complete
+  uint64_t* sempty = sfull + 1;          // [1] Stage II accumulator drained (int64 sums)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 1);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
@@ -342,7 +346,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(hempty + b, 1);
     }
     mbar_init(sfull, 1);
-    mbar_init(sempty, PAIR ? 8 : 4);    // the 4 warps of column group 0 (of each CTA) drain S
+    mbar_init(sempty, PAIR ? 2 * NUM_EPI : NUM_EPI);   // every epilogue warp (of each CTA) drains its classes
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -525,23 +529,26 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   } else if (warp == 3 && leader) {
     if (!ENC && !(DBG(8192))) {
     // ===================================================== Stage II MMA issuer (elected lane)
-    // A warp of its own: S += H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
-    // never waiting behind (or holding up) the Stage I issue loop.
+    // A warp of its own: S(t) = H(t) [Chi(t) + Clo(t)]^T goes out the moment H(t) is written,
+    // never waiting behind (or holding up) the Stage I issue loop.  Each tile's S(t) starts
+    // from zero; the epilogue drains it into exact int64 fixed-point sums (sempty) before
+    // the next tile's Stage II overwrites it, so scores do not depend on how the D-tiles of
+    // a row are split between CTAs (hence not on N or the cluster shape).
     int hb = 0, cs = 0;
     uint32_t hphase = 0, cphase = 0, sphase = 0;
-    bool seg_first = true;
     const uint32_t IDESC2 = make_idesc<0>(PAIR ? 2 * BM : BM, (int)p.Kp);
     const uint32_t d2 = tmem_base + CF::D2_COL;
     const uint32_t part_bytes = PAIR ? (uint32_t)(p.Kp * BN) : (uint32_t)(p.Kp * BN * 2);   // pair: half the classes
     for (int64_t t = t0; t < t1; ++t) {
       TWAIT(3, hfull + hb, hphase);
       TWAIT(4, cfull + cs, cphase);
-      if (seg_first) TWAIT(5, sempty, sphase ^ 1);
+      TWAIT(5, sempty, sphase ^ 1);                 // S(t - 1) drained
+      sphase ^= 1;
       tc_fence_after();
       const uint32_t c_base = smem_u32(sC + cs * CF::C_SLOT);
 #pragma unroll
       for (int s = 0; s < BN / 16; ++s) {
-        const uint32_t acc = (seg_first && s == 0) ? 0u : 1u;
+        const uint32_t acc = (s == 0) ? 0u : 1u;
 #pragma unroll
         for (int part = 0; part < 2; ++part) {      // C = hi + lo, both into the same columns
           const uint64_t bd = smem_desc_interleaved(
@@ -561,19 +568,14 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
         }
       }
-      seg_first = false;
       if constexpr (PAIR) {
         tc_commit_pair_mc_elect(hempty + hb, (uint16_t)3);
         tc_commit_pair_mc_elect(cempty + cs, (uint16_t)3);
+        tc_commit_pair_mc_elect(sfull, (uint16_t)3);
       } else {
         tc_commit_elect(hempty + hb);
         tc_commit_elect(cempty + cs);
-      }
-      if (seg_last(t, t1, p.TdG)) {
-        if constexpr (PAIR) tc_commit_pair_mc_elect(sfull, (uint16_t)3);
-        else tc_commit_elect(sfull);
-        seg_first = true;
-        sphase ^= 1;
+        tc_commit_elect(sfull);
       }
       if (++hb == NH) {
         hb = 0;
@@ -595,6 +597,59 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     unsigned long long nrecheck = 0;
     const int first_ng = (int)(t0 / p.TdG);
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    // exact per-row sums of this thread's classes (column group cq: classes cq kq .. + kq - 1)
+    // in int64 fixed point (2^-shift units): every tile's S(t) is added after it is complete
+    static_assert(NUM_CQ <= 2, "argmax exchange of two column groups");
+    constexpr int KQ_MAX = CF::KP_MAX / NUM_CQ;
+    const int kq = (int)p.Kp / NUM_CQ;               // a multiple of 8
+    long long sacc[KQ_MAX];
+#pragma unroll
+    for (int u = 0; u < KQ_MAX; ++u) sacc[u] = 0;
+    auto drain_s = [&]() {
+      TWAIT(8, sfull, sphase);
+      sphase ^= 1;
+      tc_fence_after();
+      const uint32_t sb = tmem_base + lane_off + CF::D2_COL + cq * kq;
+#pragma unroll
+      for (int c0 = 0; c0 < KQ_MAX; c0 += 8) {
+        if (c0 < kq) {
+          uint32_t r[8];
+          tmem_ld8(sb + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float v = __uint_as_float(r[j]);
+            // v 2^shift is exact (a power-of-two scaling) in fp32 when 2^shift is a normal
+            // float, so both conversions round the same exact value
+#ifdef HDC_S2_NOCVT
+            sacc[c0 + j] += (long long)__float_as_int(v);   // diagnostics: cost of the conversion (wrong sums)
+#else
+            sacc[c0 + j] += p.scale_f > 0.f ? __float2ll_rn(v * p.scale_f) : llrint((double)v * p.scale);
+#endif
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_lead(sempty);
+    };
+    // row argmax from the two column groups' (best value, lowest index) -- group 0 holds the
+    // lower classes, so it wins ties; row < 0: padding row, no label
+    float* xv = reinterpret_cast<float*>(smem + CF::OFF_X);
+    int* xi = reinterpret_cast<int*>(smem + CF::OFF_X + 4 * BM);
+    auto epi_argmax = [&](int best, float bv, int64_t row) {
+      if constexpr (NUM_CQ == 2) {
+        named_bar(1, NUM_EPI * 32);
+        if (cq == 1) {
+          xv[m] = bv;
+          xi[m] = best;
+        }
+        named_bar(1, NUM_EPI * 32);
+        if (cq == 0 && xi[m] >= 0 && (best < 0 || xv[m] > bv)) best = xi[m];
+      }
+      if (cq == 0 && row >= 0 && p.labels) p.labels[row] = best;
+    };
+    int64_t next_drain = t0;                          // next tile whose S(t) is to be added
     for (int64_t t = t0; t < t1; ++t) {
       const int ng = (int)(t / p.TdG);
       const int ni = ng * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
@@ -606,6 +661,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         while (!mbar_test(tfull + buf, bphase)) __nanosleep(500);
       }
       TWAIT(6, tfull + buf, bphase);
+      // Stage II of two tiles back: issued a whole tile ago, so complete; draining it lets the
+      // Stage II MMAs of the previous tile go out (one TMEM accumulator, drained in order)
+      if (!ENC)
+        while (next_drain <= t - 2) {
+          drain_s();
+          ++next_drain;
+        }
       const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
       if constexpr (MODE == 2) {
         TWAIT(15, cfull + cs, cphase);
@@ -791,51 +853,49 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       cs ^= 1;
       if (cs == 0) cphase ^= 1;
 
+      // ---- end of this CTA's run of D-tiles for N-tile ni: the last two tiles' S as well
       if (ENC || !seg_last(t, t1, p.TdG)) continue;
-      // ---- end of this CTA's run of D-tiles for N-tile ni: read S from TMEM.  The
-      // N-tile's D-groups are split over clusters c_first..c_last, each over its CLD ranks.
+      while (next_drain <= t) {
+        drain_s();
+        ++next_drain;
+      }
+      // ---- end of this CTA's run of D-tiles for N-tile ni: sacc = this CTA's exact sums for
+      // the row's classes of column group cq.  The N-tile's D-groups are split over clusters
+      // c_first..c_last, each over its CLD ranks; the partial sums are integers, so their
+      // total (and every score) is independent of the split.
       const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G);
       const int c_last = owner_of((int64_t)(ng + 1) * p.TdG - 1, p.T, p.G);
       const bool sole = (c_first == c_last) && CLD == 1;
-      if (cq == 0) {
-        TWAIT(8, sfull, sphase);
-        tc_fence_after();
-        const uint32_t sb = tmem_base + lane_off + CF::D2_COL;
-        const int myslot = (CLD == 1) ? ((ng == first_ng) ? 0 : 1) : (ng - first_ng);
-        float* part = p.S_part + (((int64_t)c * p.nslot + myslot) * BM + m) * p.K;
-        int best = 0;
+      const int kq0 = cq * kq;                // first class of this thread's group
+      if (sole) {
         float bv = 0.f;
-        for (int k0 = 0; k0 < K; k0 += 8) {
-          uint32_t r[8];
-          tmem_ld8(sb + k0, r);
-          float v[8];
-          tmem_ld_wait();
+        int best = -1;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int k = k0 + j;
-            if (k < K) {
-              if (sole) {
-                if (row_ok && p.scores) p.scores[row * p.K + k] = v[j];
-                if (k == 0 || v[j] > bv) {
-                  bv = v[j];
-                  best = k;
-                }
-              } else {
-                part[k] = v[j];
-              }
+        for (int u = 0; u < KQ_MAX; ++u) {
+          const int k = kq0 + u;
+          if (u < kq && k < K) {
+            const float v = (float)((double)sacc[u] * p.inv_scale);
+            if (row_ok && p.scores) p.scores[row * p.K + k] = v;
+            if (best < 0 || v > bv) {
+              bv = v;
+              best = k;
             }
           }
+          sacc[u] = 0;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_lead(sempty);
-        if (sole && row_ok && p.labels) p.labels[row] = best;
-        if (!sole) __threadfence();
+        epi_argmax(best, bv, row_ok ? row : -1);
+        continue;
       }
-      sphase ^= 1;
-      if (sole) continue;
+      const int myslot = (CLD == 1) ? ((ng == first_ng) ? 0 : 1) : (ng - first_ng);
+      {
+        long long* part = p.S_part + (((int64_t)c * p.nslot + myslot) * BM + m) * p.Kp + kq0;
+#pragma unroll
+        for (int u = 0; u < KQ_MAX; ++u) {
+          if (u < kq) part[u] = sacc[u];
+          sacc[u] = 0;
+        }
+      }
+      __threadfence();
       named_bar(1, NUM_EPI * 32);
       if (threadIdx.x == EPI_WARP0 * 32) {
         const unsigned prev = atomicAdd(p.cnt + ni, 1u);
@@ -851,7 +911,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       auto part_ptr = [&](int idx, int r, int k) {   // partial idx (cluster-major, then D rank)
         const int cc = c_first + idx / CLD, j = idx % CLD;
         const int64_t cta = (int64_t)cc * CLS + rn * CLD + j;
-        return p.S_part + ((cta * p.nslot + (cc == c_first ? slot_first : 0)) * BM + r) * p.K + k;
+        return p.S_part + ((cta * p.nslot + (cc == c_first ? slot_first : 0)) * BM + r) * p.Kp + k;
       };
       const int64_t r0 = (int64_t)ni * BM;
       const int nv = (int)((p.N - r0) < BM ? (p.N - r0) : BM);
@@ -859,32 +919,30 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (*s_flag && P > 8) {
         // Many partials (small N: the N-tile's D-range is spread over many clusters). The
         // sums go to p.scores (always non-null here), then one thread per row takes the
-        // argmax.  Few pairs: a warp per pair, lane l summing partials l, l + 32, ... in
-        // order, then a fixed butterfly.  Otherwise a thread per pair, 8 partial loads in
-        // flight, summed in partial order.  Both deterministic for a given configuration.
+        // argmax.  Few pairs: a warp per pair, lanes splitting the partials; otherwise a
+        // thread per pair, 8 partial loads in flight.  Integer sums: any order is exact.
         __threadfence();
         if (pairs <= 4 * NUM_EPI) {
           for (int pi = ew; pi < pairs; pi += NUM_EPI) {
             const int r = pi / K, k = pi - r * K;
-            float sum = 0.f;
-            for (int idx = lane; idx < P; idx += 32) sum += ld_cg(part_ptr(idx, r, k));
+            long long sum = 0;
+            for (int idx = lane; idx < P; idx += 32) sum += (long long)__ldcg(part_ptr(idx, r, k));
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (lane == 0) p.scores[(r0 + r) * p.K + k] = sum;
+            if (lane == 0) p.scores[(r0 + r) * p.K + k] = (float)((double)sum * p.inv_scale);
           }
         } else {
           for (int pi = ew * 32 + lane; pi < pairs; pi += NUM_EPI * 32) {
             const int r = pi / K, k = pi - r * K;
-            float sum = 0.f;
+            long long sum = 0;
             for (int i0 = 0; i0 < P; i0 += 8) {
-              float v[8];
+              long long v[8];
 #pragma unroll
-              for (int u = 0; u < 8; ++u) v[u] = (i0 + u < P) ? ld_cg(part_ptr(i0 + u, r, k)) : 0.f;
+              for (int u = 0; u < 8; ++u) v[u] = (i0 + u < P) ? (long long)__ldcg(part_ptr(i0 + u, r, k)) : 0ll;
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (i0 + u < P) sum = (i0 + u == 0) ? v[u] : sum + v[u];
+              for (int u = 0; u < 8; ++u) sum += v[u];
             }
-            p.scores[(r0 + r) * p.K + k] = sum;
+            p.scores[(r0 + r) * p.K + k] = (float)((double)sum * p.inv_scale);
           }
         }
         named_bar(1, NUM_EPI * 32);
@@ -900,36 +958,24 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           if (p.labels) p.labels[row] = best;
         }
-      } else if (*s_flag && cq == 0 && row_ok) {
+      } else if (*s_flag) {
         __threadfence();
-        // KC classes at a time, their partial loads independent (in flight together);
-        // per class the sum order is fixed: cluster, then D rank (bit-deterministic)
-        constexpr int KC = 16;
-        int best = 0;
+        // this thread's classes, all partials' loads of a class group in flight together
         float bv = 0.f;
-        for (int k0 = 0; k0 < K; k0 += KC) {
-          float acc[KC];
-          for (int idx = 0; idx < P; ++idx) {
-            const float* src = part_ptr(idx, m, k0);
-            float v[KC];
-#pragma unroll
-            for (int u = 0; u < KC; ++u) v[u] = (k0 + u < K) ? ld_cg(src + u) : 0.f;
-#pragma unroll
-            for (int u = 0; u < KC; ++u) acc[u] = idx == 0 ? v[u] : acc[u] + v[u];
-          }
-#pragma unroll
-          for (int u = 0; u < KC; ++u) {
-            const int k = k0 + u;
-            if (k < K) {
-              if (p.scores) p.scores[row * p.K + k] = acc[u];
-              if (k == 0 || acc[u] > bv) {
-                bv = acc[u];
-                best = k;
-              }
-            }
+        int best = -1;
+        for (int u = 0; u < kq; ++u) {
+          const int k = kq0 + u;
+          if (k >= K) break;
+          long long sum = 0;
+          for (int idx = 0; idx < P; ++idx) sum += row_ok ? (long long)__ldcg(part_ptr(idx, m, k)) : 0ll;
+          const float v = (float)((double)sum * p.inv_scale);
+          if (row_ok && p.scores) p.scores[row * p.K + k] = v;
+          if (best < 0 || v > bv) {
+            bv = v;
+            best = k;
           }
         }
-        if (p.labels) p.labels[row] = best;
+        epi_argmax(best, bv, row_ok ? row : -1);
       }
       named_bar(1, NUM_EPI * 32);     // s_flag reuse
     }
@@ -1495,6 +1541,9 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.c_tile_bytes = (uint32_t)tc_c_tile_bytes(mode, o.K);
   p.S_part = o.S_part;
   p.s_part_cap = o.s_part_slots;
+  p.scale = ldexp(1.0, o.shift);
+  p.inv_scale = ldexp(1.0, -o.shift);
+  p.scale_f = (o.shift >= -126 && o.shift <= 126) ? ldexpf(1.f, o.shift) : 0.f;
   p.cnt = o.cnt;
   p.recheck_count = o.recheck;
   p.hout = o.hout;

@@ -84,8 +84,9 @@ struct TcOperands {
   const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
   const int64_t* rowtau;             // [N_p] int8 mode
   const int64_t* coltau;             // [Dq]  int8 mode
-  float* S_part;                     // [s_part_slots][128][K]
+  long long* S_part;                 // [s_part_slots][128][Kp] int64 fixed-point partial scores
   int64_t s_part_slots;
+  int shift;                         // fixed-point shift of the Stage II sums (tc_corr_shift)
   unsigned* cnt;                     // [N_p / 128]
   unsigned long long* recheck;
   // int8 mode deferred rechecks (tc_recheck_kernel / tc_finalize_kernel)
