@@ -25,7 +25,13 @@
  *   - Non-finite inputs are not checked on the hot path; outputs are then
  *     unspecified.
  *   - Determinism: the same inputs, precision and path give bit-identical
- *     scores and labels (fixed-order reductions, no floating-point atomics).
+ *     scores and labels (fixed-order reductions; cross-CTA sums only in integers).
+ *     The tensor-core kernels (TF32 / BF16 / FP32_TC fused kernel, and the FP32_TC
+ *     small-batch kernel) add each row's per-tile Stage II scores EXACTLY, in int64
+ *     fixed point, so a row's scores and label do not depend on N, on how a batch is
+ *     split into calls or shards, or on the launch configuration.  The fp32 FFMA kernels
+ *     sum D-split partials in fp32 in an order that depends on N: their scores may differ
+ *     in the last bits between batch sizes (labels only at near-ties).
  *   - A model handle is immutable after creation but owns a workspace: calls on
  *     ONE handle must be serialised (one stream at a time); use one handle per
  *     concurrent stream.
@@ -116,7 +122,9 @@ hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int3
  * staging buffers, so back-to-back calls pipeline: the copy of call i + 1 overlaps
  * the inference of call i.  For N > 32 the rows are also processed in up to 8
  * chunks of ~8192, the copy of chunk j + 1 overlapping the inference of chunk j
- * (rows are independent, so results equal the one-shot call).
+ * (rows are independent: on the tensor-core kernels the results equal the
+ * one-shot call bit for bit; on the fp32 FFMA kernels up to fp32 summation order, see
+ * Determinism above).
  * Ordering: the copies of X_host are ordered after this model's previous host-path
  * calls, NOT after other work already queued on `stream` -- X_host must be fully
  * written when the call is made.  Labels / scores are written in `stream` order:

@@ -36,6 +36,19 @@ hdc_status_t cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// Every call on a model runs on the model's device (its buffers and workspaces live there),
+// whatever device is current; the caller's current device is restored on return.
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev && cudaSetDevice(dev) == cudaSuccess) switched = true;
+  }
+  ~DeviceGuard() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
+
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr int64_t kMaxF = int64_t(1) << 20;
@@ -576,6 +589,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
 
 hdc_status_t hdc_model_destroy(hdc_model_t m) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  DeviceGuard dg(m->device);
   cudaDeviceSynchronize();
   free_model_memory(m);
   delete m;
@@ -596,6 +610,7 @@ hdc_status_t hdc_model_infer_path(hdc_model_t m, const float* X, int64_t N, int3
                                   float* scores, hdc_path_t path, void* stream) {
   hdc_status_t st = validate_call(m, X, N, labels, scores);
   if (st != HDC_OK) return st;
+  DeviceGuard dg(m->device);
   if (path < HDC_PATH_AUTO || path > HDC_PATH_FUSED) return fail(HDC_ERR_INVALID_VALUE, "bad path");
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
@@ -611,6 +626,7 @@ hdc_status_t hdc_model_partial_scores(hdc_model_t m, const float* X, int64_t N, 
                                       void* stream) {
   hdc_status_t st = validate_call(m, X, N, S_partial, nullptr);
   if (st != HDC_OK) return st;
+  DeviceGuard dg(m->device);
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return cuda_fail(pe, "pending CUDA error");
   return run(m, X, N, nullptr, S_partial, HDC_PATH_AUTO, (cudaStream_t)stream);
@@ -629,6 +645,7 @@ hdc_status_t hdc_model_infer_dshard(hdc_model_t m, const float* X, int64_t N, in
                                     uint32_t epoch, void* stream) {
   hdc_status_t st = validate_call(m, X, N, labels, scores);
   if (st != HDC_OK) return st;
+  DeviceGuard dg(m->device);
   if (N < 1 || N > kSmallMaxN) return fail(HDC_ERR_UNSUPPORTED, "D-shard exchange: 1 <= N <= 32");
   if (world < 1 || rank < 0 || rank >= world) return fail(HDC_ERR_INVALID_VALUE, "rank / world");
   if (!xbufs || !aligned(xbufs, 8)) return fail(HDC_ERR_INVALID_VALUE, "null or misaligned xbufs");
@@ -655,6 +672,7 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
                                   int32_t* labels_host, float* scores_host, void* stream) {
   hdc_status_t st = validate_call(m, X_host, N, labels_host, scores_host);
   if (st != HDC_OK) return st;
+  DeviceGuard dg(m->device);
   if (N == 0) return HDC_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (N > m->Xdev_rows) {
@@ -749,6 +767,7 @@ hdc_status_t hdc_model_infer_host(hdc_model_t m, const float* X_host, int64_t N,
 hdc_status_t hdc_model_encode(hdc_model_t m, const float* X, int64_t N, uint32_t* H, int64_t ldw,
                               void* stream) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  DeviceGuard dg(m->device);
   if (N < 0) return fail(HDC_ERR_INVALID_VALUE, "N < 0");
   if (N >= (int64_t(1) << 31)) return fail(HDC_ERR_UNSUPPORTED, "N >= 2^31");
   if (N > 0 && (!X || !H)) return fail(HDC_ERR_INVALID_VALUE, "null X or H");
@@ -828,6 +847,7 @@ hdc_status_t hdc_infer(const float* X, const float* B, const float* C, int64_t N
 
 int64_t hdc_model_recheck_count(hdc_model_t m) {
   if (!m) return -1;
+  DeviceGuard dg(m->device);
   unsigned long long v = 0;
   cudaDeviceSynchronize();
   if (cudaMemcpy(&v, m->recheck, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
@@ -840,6 +860,7 @@ int32_t hdc_model_last_kernel(hdc_model_t m) { return m ? m->last_kernel : -1; }
 
 hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");
+  DeviceGuard dg(m->device);
   if (enable && !m->ev0) {
     if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess)
       return fail(HDC_ERR_CUDA, "event creation");
@@ -850,6 +871,7 @@ hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable) {
 
 float hdc_model_last_kernel_ms(hdc_model_t m) {
   if (!m || !m->timing || !m->ev0) return -1.f;
+  DeviceGuard dg(m->device);
   if (cudaEventSynchronize(m->ev1) != cudaSuccess) return -1.f;
   float ms = -1.f;
   if (cudaEventElapsedTime(&ms, m->ev0, m->ev1) != cudaSuccess) return -1.f;

@@ -38,6 +38,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1302,8 +1303,13 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // persistent: as many clusters as can be co-resident (148 SMs: 74 pairs, 33 quads);
-  // computed once per instantiation (thread-safe static initialisation)
-  static const int max_clusters = [&]() {
+  // computed once per instantiation and device (benign race: every thread computes the same)
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> cache[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int max_clusters = (dev >= 0 && dev < kMaxDev) ? cache[dev].load() : 0;
+  if (max_clusters <= 0) {
     cudaLaunchConfig_t q = cfg;
     q.gridDim = dim3(CLS * (num_sms / CLS), 1, 1);
     int n = 0;
@@ -1313,8 +1319,9 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
       cudaGetLastError();
       n = num_sms / CLS;
     }
-    return n;
-  }();
+    max_clusters = n;
+    if (dev >= 0 && dev < kMaxDev) cache[dev].store(n);
+  }
   p.G = (int)(p.T < max_clusters ? p.T : max_clusters);
   const int64_t per = (p.T + p.G - 1) / p.G;    // cluster tiles per range (at most)
   p.nslot = (CLD == 1) ? 2 : (int)((per + p.TdG - 1) / p.TdG + 1);

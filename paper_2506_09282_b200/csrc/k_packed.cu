@@ -166,7 +166,8 @@ __global__ void label_sort_kernel(const int32_t* __restrict__ y, int64_t N, int6
 constexpr int kBundleRows = 128;
 __global__ void bundle_kernel(const uint32_t* __restrict__ H, int64_t ldw, int64_t N, int64_t D,
                               const int32_t* __restrict__ y, const int64_t* __restrict__ perm,
-                              int32_t* __restrict__ counts) {
+                              int32_t* __restrict__ counts, const unsigned* __restrict__ err) {
+  if (*err) return;                    // a label outside [0, K): leave counts untouched
   const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t i0 = (int64_t)blockIdx.y * kBundleRows;
   const int64_t i1 = (i0 + kBundleRows) < N ? (i0 + kBundleRows) : N;
@@ -200,7 +201,9 @@ __global__ void bundle_kernel(const uint32_t* __restrict__ H, int64_t ldw, int64
 }
 
 // constrained bundling: m = HardSign(count) (ties -> +1)
-__global__ void hardsign_i32_kernel(const int32_t* __restrict__ counts, int64_t n, float* __restrict__ M) {
+__global__ void hardsign_i32_kernel(const int32_t* __restrict__ counts, int64_t n, float* __restrict__ M,
+                                    const unsigned* __restrict__ err) {
+  if (*err) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     M[i] = counts[i] >= 0 ? 1.f : -1.f;
 }
@@ -240,11 +243,11 @@ cudaError_t launch_bundle(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, 
   e = cudaGetLastError();
   if (e == cudaSuccess) {
     dim3 grid((unsigned)((ldw + 127) / 128), (unsigned)((N + kBundleRows - 1) / kBundleRows));
-    if (N > 0) bundle_kernel<<<grid, 128, 0, st>>>(H, ldw, N, D, y, perm, counts);
+    if (N > 0) bundle_kernel<<<grid, 128, 0, st>>>(H, ldw, N, D, y, perm, counts, err);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess && M) {
-    hardsign_i32_kernel<<<148 * 4, 256, 0, st>>>(counts, K * D, M);
+    hardsign_i32_kernel<<<148 * 4, 256, 0, st>>>(counts, K * D, M, err);
     e = cudaGetLastError();
   }
   cudaFreeAsync(offs, st);

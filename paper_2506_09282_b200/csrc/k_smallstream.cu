@@ -458,12 +458,16 @@ cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
   const size_t sm = stream_smem(nst, p.F, NB, p.K, p.max_cols);
   if (sm > lim) return cudaErrorInvalidValue;
   p.nst = nst;
-  static std::atomic<size_t> attr_set{0};      // host-side attribute call only when it grows
-  if (sm > attr_set.load()) {
+  // the attribute is per device context: set once per device (host call only then)
+  constexpr int kMaxDev = 64;
+  static std::atomic<size_t> attr_set[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev || sm > attr_set[dev].load()) {
     cudaError_t e = cudaFuncSetAttribute(smallstream_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lim);
     if (e != cudaSuccess) return e;
-    attr_set = lim;
+    if (dev >= 0 && dev < kMaxDev) attr_set[dev] = lim;
   }
   static unsigned long long* dbg = nullptr;
   const bool debug = getenv("HDC_SMALL_DEBUG") != nullptr;

@@ -162,3 +162,23 @@ def test_encode_full_size_cfg2_rows(hdc):
     rows = np.r_[0:64, cfg.N - 64:cfg.N, np.random.default_rng(1).integers(0, cfg.N, 64)]
     Hg = _unpack(hdc, H[torch.from_numpy(rows).cuda()], cfg.D)
     assert np.array_equal(Hg, oracle.encode(X[rows], B))
+
+
+def test_bundle_rejects_bad_labels_without_touching_counts(hdc):
+    # validation happens on the device before any accumulation: on HDC_ERR_INVALID_VALUE the
+    # caller's counts (and M) are exactly as they were
+    rng = np.random.default_rng(5)
+    N, D, K = 300, 700, 4
+    H = torch.from_numpy(rng.integers(0, 2 ** 31, (N, (D + 31) // 32), dtype=np.int64).astype(np.int32)).cuda()
+    y = torch.from_numpy(rng.integers(0, K, N).astype(np.int32)).cuda()
+    y[17] = K                                              # out of range
+    counts = torch.arange(K * D, dtype=torch.int32, device="cuda").reshape(K, D)
+    before = counts.clone()
+    with pytest.raises(hdc.HDCError):
+        hdc.bundle_classes(H, D, y, K, counts=counts)
+    torch.cuda.synchronize()
+    assert torch.equal(counts, before)
+    y[17] = -1
+    with pytest.raises(hdc.HDCError):
+        hdc.bundle_classes(H, D, y, K, counts=counts)
+    assert torch.equal(counts, before)
