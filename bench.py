@@ -337,11 +337,13 @@ def run_ours(args, rank, world, local_rank):
     B = torch.from_numpy(Bh).to(dev)
     C = torch.from_numpy(Ch).to(dev)
     model = hdc.Model(B, C, prec=args.prec)
-    counts = [hi - lo for lo, hi in (shard_bounds(cfg.N, world, r) for r in range(world))]
-    n_pad = max(counts) if strong else n_local
-    lab_pad = torch.zeros(n_pad, dtype=torch.int32, device=dev)      # this rank's labels
-    labels = lab_pad[:n_local]
-    lab_all = torch.empty(n_pad * world, dtype=torch.int32, device=dev) if (strong and world > 1) else None
+    gather = None
+    if strong and world > 1:
+        from paper_2506_09282_b200.sharding import NShardGather
+        gather = NShardGather(cfg.N, device=dev)             # the N-shard's label all-gather
+        labels = gather.labels
+    else:
+        labels = torch.zeros(n_local, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     Sbuf = torch.empty(cfg.N, cfg.K, dtype=torch.float32, device=dev)
     Hbuf = torch.empty(n_local, (cfg.D + 31) // 32, dtype=torch.int32, device=dev)
@@ -373,8 +375,8 @@ def run_ours(args, rank, world, local_rank):
             hdc.argmax(Sbuf, labels=labels)
         else:
             model.infer(X, labels=labels, path=args.path)
-            if lab_all is not None:                  # N-shard: gather every rank's labels
-                dist.all_gather_into_tensor(lab_all, lab_pad)
+            if gather is not None:                   # N-shard: gather every rank's labels
+                gather.gather()
 
     run_peaks = {} if args.no_peaks else probe_peaks(dev)
     # L2 flush between timed steps (untimed): write a 2x L2 buffer, then READ another one,

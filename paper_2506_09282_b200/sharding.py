@@ -5,8 +5,9 @@ Two partitions, following the paper's two Stage II variants:
 * N-shard (ScalableHD-L, Alg. 4, text P:410): rows of X are split
   across ranks; B and C are replicated; each rank runs the whole fused path on
   its rows; the only collective is an all-gather of the int32 labels (and,
-  optionally, scores).  Rows are independent, so labels equal the single-GPU
-  labels bit for bit when the per-row arithmetic does not depend on the shard.
+  optionally, scores).  Rows are independent and the tensor-core kernels sum each
+  row's Stage II tiles exactly (int64), so labels and scores equal the single-GPU ones
+  bit for bit (tests/test_gpu_nshard.py); the fp32 FFMA kernels up to fp32 order.
 
 * D-shard (ScalableHD-S, Alg. 3, text P:355): rank r holds the column
   slice D_r of B and C; it computes the partial scores S_r = HardSign(X B_r) C_r^T
@@ -69,6 +70,33 @@ def shard_n_infer(model, X_local, N_total, return_scores=False, group=None):
     return labels, scores
 
 
+class NShardGather:
+    """The N-shard's one collective as the benchmark times it: every rank's int32 labels
+    into one preallocated buffer with a single ``all_gather_into_tensor`` (shards padded to
+    the largest, ScalableHD-L's "write y^(t') to global", Alg. 4).  ``labels`` is this
+    rank's label buffer (write the shard's labels into it), ``gather()`` enqueues the
+    collective and ``result()`` returns the N_total labels in row order."""
+
+    def __init__(self, N_total, group=None, device=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.N = N_total
+        self.bounds = [shard_bounds(N_total, self.world, r) for r in range(self.world)]
+        self.counts = [hi - lo for lo, hi in self.bounds]
+        self.pad = max(self.counts) if self.counts else 0
+        self.buf = torch.zeros(self.pad, dtype=torch.int32, device=device)
+        self.labels = self.buf[: self.counts[self.rank]]
+        self.out = torch.empty(self.pad * self.world, dtype=torch.int32, device=device)
+
+    def gather(self):
+        dist.all_gather_into_tensor(self.out, self.buf, group=self.group)
+        return self.out
+
+    def result(self):
+        return torch.cat([self.out[r * self.pad: r * self.pad + c] for r, c in enumerate(self.counts)])
+
+
 def shard_d_infer(model_slice, X, argmax_fn, return_scores=False, group=None):
     """D-shard inference: `model_slice` holds this rank's columns of B and C;
     X is replicated.  All-reduce(SUM) of the N x K partial scores, then argmax."""
@@ -85,7 +113,8 @@ class DShardExchange:
     every rank's buffer is mapped into every process; the device array of the `world`
     buffer addresses is what the kernel writes through.  ``n_max`` bounds the batch
     rows (<= 32), ``K`` is the class count.  Collective: all ranks construct it together
-    and then call :meth:`infer` the same number of times with the same X shape."""
+    and then call :meth:`infer` the same number of times, each call with the same X on
+    every rank (N may change from call to call: the slots are sized for 32 rows)."""
 
     def __init__(self, n_max, K, group=None, device=None):
         import torch.distributed._symmetric_memory as symm

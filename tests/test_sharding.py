@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2506_09282_b200.sharding import d_shard_slices, shard_bounds, shard_d_infer, shard_n_infer
+from paper_2506_09282_b200.sharding import NShardGather, d_shard_slices, shard_bounds, shard_d_infer, shard_n_infer
 
 
 class OracleRankModel:
@@ -60,7 +60,12 @@ def _worker(rank, world, port, q):
         m = OracleRankModel(np.ascontiguousarray(B[:, dlo:dhi]), np.ascontiguousarray(C[:, dlo:dhi]))
         yd, Sd = shard_d_infer(m, torch.from_numpy(X), lambda s: torch.argmax(s, dim=1).to(torch.int32),
                                return_scores=True)
-        q.put((rank, y.numpy(), S.numpy(), yd.numpy(), Sd.numpy()))
+        # the benchmark's gather: shard labels into the padded buffer, one all_gather
+        g = NShardGather(N)
+        yl, _ = OracleRankModel(B, C).infer(torch.from_numpy(X[lo:hi]))
+        g.labels.copy_(yl)
+        g.gather()
+        q.put((rank, y.numpy(), S.numpy(), yd.numpy(), Sd.numpy(), g.result().numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -80,7 +85,7 @@ def test_shard_bounds_partition():
     assert sum(widths) == 10000 and all(w % 4 == 0 for w in widths)
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_gloo_world2_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -94,7 +99,8 @@ def test_gloo_world2_matches_single_process(world):
         assert p.exitcode == 0
     X, B, C = _inputs()
     full = oracle.infer(X, B, C)
-    for rank, y, S, yd, Sd in res:
+    for rank, y, S, yd, Sd, yg in res:
+        assert np.array_equal(yg, full["y"])          # NShardGather: every row, in order
         # N-shard: rows are independent -> bit-identical to one process
         assert np.array_equal(y, full["y"]) and np.array_equal(S, full["S"])
         # D-shard: sum of partial scores equals the full scores up to float64 rounding
