@@ -260,7 +260,7 @@ def probe_peaks(dev):
     return out
 
 
-def roofline_for(cfg, prec, path, ms_kernel, peaks, run_peaks, units):
+def roofline_for(cfg, prec, path, ms_kernel, peaks, run_peaks, units, kernel=None):
     """Roofline object of the dominant kernel: algorithmic work per launch
     / measured kernel time against the peak of the contraction's own dtype."""
     N, F, D, K = units, cfg.F, cfg.D, cfg.K
@@ -278,6 +278,8 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, run_peaks, units):
     bf16 = float(peaks["bf16_tflops"])
     out = {"unit": "TFLOP/s", "traffic": None, "algorithmic_per_launch": flops,
            "algorithmic_unit": "FLOP: 2 N F D + 2 N D K"}
+    if prec == "fp32" and kernel == "tc":
+        prec = "fp32_tc"                               # fp32 semantics served by the int8 kernels
     if prec == "fp32":
         mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak = N_SM * 128 * 2 * mhz * 1e6 / 1e12       # FFMA: 148 SM x 128 lanes x 2 flop
@@ -515,7 +517,7 @@ def run_ours(args, rank, world, local_rank):
     path = args.path
     if path == "auto":
         path = "small" if kernel in ("small", "small_tc") else "fused"
-    roof = roofline_for(cfg, args.prec, path, kernel_ms, peaks, run_peaks, n_local)
+    roof = roofline_for(cfg, args.prec, path, kernel_ms, peaks, run_peaks, n_local, kernel)
     roof["peak_source"] = peaks_src
     roof["traffic"] = measured_traffic(cfg.name, args.prec)
     if roof["traffic"] is not None:

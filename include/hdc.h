@@ -57,10 +57,12 @@ typedef enum {
 } hdc_status_t;
 
 /* Arithmetic of Stage I.  The paper keeps B and M in fp32.
- *   HDC_PREC_FP32: fp32 FFMA accumulation + float64 re-evaluation of every
- *     pre-activation whose |v| is within the rigorous fp32 error bound
- *     (F+32) 2^-24 ||x_n|| ||b_d||, so each HardSign decision equals the one
- *     of the exact product X B (DESIGN.md §4 "sign recheck").
+ *   HDC_PREC_FP32: HardSign decisions equal those of the exact product X B.  Served by
+ *     the HDC_PREC_FP32_TC kernels below (same guarantee, ~12x faster) when K <= 32 and
+ *     F <= 100000, else -- or when the environment variable HDC_FP32_FFMA is set at
+ *     hdc_model_create -- by the fp32 FFMA kernels: fp32 FFMA accumulation + float64
+ *     re-evaluation of every pre-activation whose |v| is within the rigorous fp32 error
+ *     bound (F+32) 2^-24 ||x_n|| ||b_d|| (DESIGN.md §4 "sign recheck").
  *   HDC_PREC_TF32 / HDC_PREC_BF16: Stage I on tcgen05 tensor cores with X and B
  *     rounded to tf32 (RNA) / bf16 (RN), fp32 accumulation; no recheck
  *     (approximate H).  Stage II on tcgen05 with C split into bf16 hi + lo.

@@ -39,12 +39,16 @@ CASES = [  # (prec, path, N, F, D, K, cluster)
     ("fp32", "fused", 131, 75, 300, 10, None), ("fp32", "small", 31, 90, 515, 6, None),
     ("fp32_tc", "small", 17, 784, 1234, 10, None), ("fp32_tc", "small", 3, 5, 9, 2, None),
     ("bf16", "small", 8, 100, 700, 4, None), ("fp32_tc", "auto", 1, 1, 1, 1, None),
+    ("fp32", "fused", 131, 75, 300, 10, "ffma"), ("fp32", "small", 31, 90, 515, 6, "ffma"),
+    ("fp32", "small", 9, 3000, 300, 6, "ffma"),
 ]
 
 
 @pytest.mark.parametrize("prec,path,N,F,D,K,cluster", CASES)
 def test_outputs_stay_in_bounds(hdc, monkeypatch, prec, path, N, F, D, K, cluster):
-    if cluster:
+    if cluster == "ffma":
+        monkeypatch.setenv("HDC_FP32_FFMA", "1")       # the fp32 FFMA / streaming kernels
+    elif cluster:
         monkeypatch.setenv("HDC_TC_CLUSTER", cluster)
     monkeypatch.setenv("HDC_SMALL_TC", "1")
     rng = np.random.default_rng(N * 31 + F * 7 + D + K)

@@ -17,6 +17,13 @@ from tests.gpu_util import check_result, parity_fp32, run_model, to_dev
 
 pytestmark = pytest.mark.gpu
 
+@pytest.fixture(autouse=True)
+def _fp32_on_ffma(monkeypatch):
+    # fp32 models in this module exercise the fp32 FFMA kernels (HDC_PREC_FP32 otherwise
+    # runs on the int8 tensor-core kernels when eligible, tested elsewhere)
+    monkeypatch.setenv("HDC_FP32_FFMA", "1")
+
+
 
 @pytest.fixture(scope="module")
 def hdc(cuda_device):

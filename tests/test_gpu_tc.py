@@ -56,14 +56,16 @@ def test_tc_exact_cancellations_and_zero_rows(hdc):
     m.close()
 
 
-def test_tc_int8_matches_ffma_labels(hdc):
+def test_tc_int8_matches_ffma_labels(hdc, monkeypatch):
     cfg = CONFIGS["cfg1"]
     X, B, C = make_X(cfg), make_B(cfg), make_C(cfg)
     Bd, Cd = to_dev(B, C)
     m1 = hdc.Model(Bd, Cd, prec="fp32_tc")
+    monkeypatch.setenv("HDC_FP32_FFMA", "1")            # m2 on the fp32 FFMA kernel
     m2 = hdc.Model(Bd, Cd, prec="fp32")
     y1, S1 = run_model(m1, X, "fused")
     y2, S2 = run_model(m2, X, "fused")
+    assert m2.last_kernel() == "ffma"
     # both sign-exact -> identical H -> same labels; same Stage II order -> same scores
     assert np.array_equal(y1, y2)
     assert np.max(np.abs(S1 - S2)) < 1e-4
