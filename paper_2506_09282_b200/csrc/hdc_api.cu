@@ -97,6 +97,7 @@ struct hdc_model_s {
   float* bnorm = nullptr;
   // small-batch workspace
   unsigned long long* acc_t = nullptr;   // K2t: [32][K] int64 fixed-point score accumulators
+  unsigned long long* acc_s = nullptr;   // K2s: the same for the fp32 streaming kernel
   unsigned* cnt_t = nullptr;             // K2t: [1] arrival counter
   uint8_t* ximg_t = nullptr;             // K2t: X limb image
   float* S_part = nullptr;
@@ -145,6 +146,8 @@ struct hdc_model_s {
     SmallWorkspace w;
     w.S_part = S_part;
     w.cnt1 = cnt;
+    w.acc = acc_s;
+    w.shift = corr_shift;
     w.recheck = recheck;
     return w;
   }
@@ -191,6 +194,7 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->bnorm);
   cudaFree(m->S_part);
   cudaFree(m->acc_t);
+  cudaFree(m->acc_s);
   cudaFree(m->cnt_t);
   cudaFree(m->ximg_t);
   cudaFree(m->cnt);
@@ -535,6 +539,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
   ALLOC(m->cnt, sizeof(unsigned) * 64);
   ALLOC(m->recheck, sizeof(unsigned long long));
+  ALLOC(m->acc_s, sizeof(unsigned long long) * kSmallMaxN * K);
 #undef ALLOC
   if (e != cudaSuccess) {
     free_model_memory(m);
@@ -553,6 +558,11 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
                               : cudaMemset(m->Cp, 0, sizeof(float) * K * m->Dp);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 64);
+  if (e == cudaSuccess) e = cudaMemset(m->acc_s, 0, sizeof(unsigned long long) * kSmallMaxN * K);
+  // fixed point of the exact cross-CTA score sums (all models) and of the int8 recheck
+  // corrections: 2 D max|C| 2^shift < 2^62
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
   const int mode = tc_mode_of(m);
   const int64_t tn = tc_tile_n(mode < 0 ? 0 : mode, K);
   tc_cluster_shape(mode < 0 ? 0 : mode, K, F, D, &m->cl_n, &m->cl_d, &m->cl_virt);
@@ -570,10 +580,6 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
     }
     if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Dq, m->Cil, st0);
-    // fixed point of the exact Stage II sums (all tensor-core modes) and of the int8 mode's
-    // recheck corrections
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
     if (e == cudaSuccess && mode == 2) {
       // K2t (small-batch tensor-core kernel) accumulators, zero between launches
       if (e == cudaSuccess) e = cudaMalloc((void**)&m->acc_t, sizeof(unsigned long long) * kSmallMaxN * K);

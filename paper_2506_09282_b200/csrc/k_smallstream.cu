@@ -59,7 +59,9 @@ struct StreamParams {
   int nst;               // ring stages per consumer warp
   int max_cols;          // columns of the largest CTA range (4 ceil(units / G))
   int64_t units;
-  float* S_part;         // [G + groups][NB][K]
+  float* S_part;         // [G + groups][NB][K] (unused: partials go to acc)
+  unsigned long long* acc;   // [32][K] int64 fixed-point score sums, zero between launches
+  double scale, inv_scale;   // 2^shift, 2^-shift
   unsigned* cnt;         // [1 + groups], zero between launches
   unsigned long long* recheck_count;
   float* scores;
@@ -315,83 +317,38 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   SS_MARK(2);
   cbar();
 
-  // ---- CTA S_local = per-warp partials in warp order; the last-arriving CTA sums the
-  // G partials (all loads in flight at once) in a fixed order and takes the argmax
+  // ---- CTA S_local = per-warp partials in warp order, converted to int64 fixed point
+  // (2^-shift units) and added across CTAs with integer atomics: exact and order-free
+  // (Alg. 3 `S += S_local`), so the last CTA only converts the N x K sums
   const int nk = p.nrows * K;
-  const int pst = (NB * K + 3) & ~3;               // partial stride (float4 aligned)
-  float* mypart = p.S_part + (int64_t)c * pst;
   for (int i = tid; i < nk; i += kCt) {
     float a = Sw[i];
     for (int w = 1; w < kCw; ++w) a += Sw[(size_t)w * NB * K + i];
-    mypart[i] = a;
+    atomicAdd(p.acc + i, (unsigned long long)llrint((double)a * p.scale));
   }
-  __threadfence();
   cbar();
   SS_MARK(3);
   if (tid == 0) {
-    const unsigned prev = atomicAdd(p.cnt, 1u);
+    unsigned prev;   // release: this CTA's additions are ordered before its arrival is counted
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt) : "memory");
     s_last = (prev == (unsigned)(p.G - 1)) ? 1 : 0;
-    if (s_last) p.cnt[0] = 0u;
+    if (s_last) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p.cnt) : "memory");
+      (void)v;
+      p.cnt[0] = 0u;
+    }
   }
   cbar();
   if (!s_last) return;
-  __threadfence();
-  // thread layout: kCt threads = P partial-lanes x Q4 output quads; lane j sums partials
-  // j, j + P, ... in order (float4 loads, 8 in flight), then the P lane sums in a fixed order
   float* Sfin = fin;                                  // [nk]
-  float4* tmp = reinterpret_cast<float4*>(fin + ((nk + 31) & ~31));   // [P][Q4]
-  const int nq = (nk + 3) / 4;
-  const int P = nq >= kCt ? 1 : (nq >= kCt / 2 ? 2 : (nq >= kCt / 4 ? 4 : (nq >= kCt / 8 ? 8 :
-                (nq >= kCt / 16 ? 16 : 32))));
-  const int Q4 = kCt / P;
-  for (int q0 = 0; q0 < nq; q0 += Q4) {
-    const int j = tid / Q4, q = q0 + tid % Q4;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q < nq) {
-      constexpr int BATCH = 8;
-      for (int cc0 = j; cc0 < p.G; cc0 += P * BATCH) {
-        float4 v[BATCH];
-#pragma unroll
-        for (int b = 0; b < BATCH; ++b) {
-          const int cc = cc0 + b * P;
-          v[b] = cc < p.G ? __ldcg(reinterpret_cast<const float4*>(p.S_part + (int64_t)cc * pst) + q)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int b = 0; b < BATCH; ++b)
-          if (cc0 + b * P < p.G) {
-            if (cc0 == j && b == 0) a = v[b];
-            else {
-              a.x += v[b].x;
-              a.y += v[b].y;
-              a.z += v[b].z;
-              a.w += v[b].w;
-            }
-          }
-      }
-      tmp[j * Q4 + (q - q0)] = a;
-    }
-    cbar();
-    if (tid < Q4 && q0 + tid < nq) {
-      float4 t = tmp[tid];
-      for (int jj = 1; jj < P; ++jj) {
-        const float4 u = tmp[jj * Q4 + tid];
-        t.x += u.x;
-        t.y += u.y;
-        t.z += u.z;
-        t.w += u.w;
-      }
-      const float tv[4] = {t.x, t.y, t.z, t.w};
-      for (int i = 0; i < 4; ++i) {
-        const int e = 4 * (q0 + tid) + i;
-        if (e < nk) {
-          Sfin[e] = tv[i];
-          if (p.scores) p.scores[e] = tv[i];
-        }
-      }
-    }
-    cbar();
+  for (int i = tid; i < nk; i += kCt) {
+    const long long a = (long long)atomicExch(p.acc + i, 0ull);   // read and reset for the next call
+    const float v = (float)((double)a * p.inv_scale);
+    Sfin[i] = v;
+    if (p.scores) p.scores[i] = v;
   }
+  cbar();
   SS_MARK(4);
   if (p.xworld > 0) {
     // ---- D-shard exchange over peer memory (Alg. 3 `S += S_local`, across GPUs):
@@ -525,6 +482,9 @@ cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, con
   p.nst = 0;
   p.S_part = ws.S_part;
   p.cnt = ws.cnt1;
+  p.acc = ws.acc;
+  p.scale = ldexp(1.0, ws.shift);
+  p.inv_scale = ldexp(1.0, -ws.shift);
   p.recheck_count = ws.recheck;
   p.scores = scores;
   p.labels = labels;

@@ -28,6 +28,8 @@ struct SmallWorkspace {
   float* S_part;         // [num_sms][32][K]
   unsigned* cnt1;        // [64] last-arriver counters, zero between launches
   unsigned long long* recheck;  // fp64 re-evaluation counter (diagnostic)
+  unsigned long long* acc;      // [32][K] int64 fixed-point score sums (K2s), zero between launches
+  int shift;                    // fixed point: 2^-shift units (tc_corr_shift)
 };
 
 int64_t small_num_ctas(int64_t D, int num_sms);                       // CTAs of K2
