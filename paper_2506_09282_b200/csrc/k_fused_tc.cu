@@ -1343,6 +1343,7 @@ cudaError_t launch_cluster_k(int cl_n, int cl_d, int virt, const CUtensorMap& a,
   if (virt) {
     if (cl_n == 1 && cl_d == 4) return launch_mode<MODE, BN, 1, 4, ENC, false, false, KW>(a, b, c, p, num_sms, st);
     if (cl_n == 1 && cl_d == 8) return launch_mode<MODE, BN, 1, 8, ENC, false, false, KW>(a, b, c, p, num_sms, st);
+    if (cl_n == 1 && cl_d == 16) return launch_mode<MODE, BN, 1, 16, ENC, false, false, KW>(a, b, c, p, num_sms, st);
     return cudaErrorInvalidValue;
   }
   if (cl_n == 1 && cl_d == 1) return launch_mode<MODE, BN, 1, 1, ENC, true, false, KW>(a, b, c, p, num_sms, st);
@@ -1397,7 +1398,7 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   // default: CTA pairs on two N-tiles of the same D-tile, multicasting the B tile
   // (measured best of 1x1 / 1x2 / 2x1 / 2x2 / 1x4 hardware clusters at cfg2, tools/tc_timing.py).
   // When the live X tiles of 148 CTAs plus B exceed the L2 (large F: cfg5 read 176 GB from
-  // DRAM per launch), a virtual 1 x g group puts g CTAs on each N-tile (g = 4, 8).
+  // DRAM per launch), a virtual 1 x g group puts g CTAs on each N-tile (g = 4, 8, 16).
   const int bn = tile_n_for(mode, K);
   int n = 2, d = 1, v = 0;
   if (bn == 80 && mode != 2) n = 1;               // (bf16/tf32 with K > 32: no cluster)
@@ -1408,7 +1409,10 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   if (148.0 * a_tile + b_all > l2) {
     n = 1;
     v = 1;
-    d = (37.0 * a_tile + b_all <= l2) ? 4 : 8;
+    // group size g: the g-CTA groups' live X tiles plus B should leave L2 headroom
+    // (measured at cfg5: 1x16 20.4 ms vs 1x8 21.1-21.8 ms int8, 6.51 vs 6.68 ms bf16)
+    const double fit = 75e6;
+    d = (37.0 * a_tile + b_all <= fit) ? 4 : (18.0 * a_tile + b_all <= fit) ? 8 : 16;
   }
   const char* env = getenv("HDC_TC_CLUSTER");
   int en = 0, ed = 0;
@@ -1416,7 +1420,7 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   if (env) {
     const int got = sscanf(env, "%dx%d%c", &en, &ed, &vc);
     if (got >= 2 && !(bn == 80 && mode != 2)) {
-      if (got == 3 && vc == 'v' && en == 1 && (ed == 4 || ed == 8)) {
+      if (got == 3 && vc == 'v' && en == 1 && (ed == 4 || ed == 8 || ed == 16)) {
         n = 1; d = ed; v = 1;
       } else if (got == 3 && vc == 'p' && en == 2 && ed == 1) {
         n = 2; d = 1; v = 2;                      // CTA pair (cta_group::2)
