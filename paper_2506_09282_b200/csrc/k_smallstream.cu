@@ -129,9 +129,17 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
 
   if (warp == kCw) {
     // ===================================================== producer: lane w streams warp w's units
-    if (lane == kCw) {          // X, one bulk copy, issued first
-      mbar_arrive_expect_tx(xfull, xbytes);
+    if (lane == kCw) {
+      // X (one bulk copy), this CTA's C columns (one per class) and ||b_d||, issued before
+      // any of B so they are first in the memory queues (consumer loads issued at the same
+      // time would wait behind the B stream)
+      const int ncol_p = (int)(u1 - u0) * 4;
+      const int64_t col0_p = u0 * 4;
+      mbar_arrive_expect_tx(xfull, xbytes + (uint32_t)((K + 1) * ncol_p * 4));
       bulk_load(Xraw, reinterpret_cast<const void*>(xaddr & ~uint64_t(15)), xbytes, xfull);
+      for (int k = 0; k < K; ++k)
+        bulk_load(Cs + (size_t)k * ncol_p, p.Cp + (int64_t)k * p.Dp + col0_p, (uint32_t)(ncol_p * 4), xfull);
+      bulk_load(bns, p.bnorm + col0_p, (uint32_t)(ncol_p * 4), xfull);
     }
     if (lane < kCw) {
       const int w = lane;
@@ -154,31 +162,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   }
 
   // ===================================================== consumers
-  // Stage X (nrows x F) -> Xs[f][n], this CTA's columns of C -> Cs[k][cols] and of ||b_d||
-  // -> bns, all loads of a batch issued before any store (one HBM latency per batch),
-  // while the producer's first chunks are already in flight.
+  // X, this CTA's columns of C (Cs[k][cols]) and of ||b_d|| (bns) arrive by the producer's
+  // bulk copies (xfull), ahead of the B stream
   const int ncol = (int)(u1 - u0) * 4;
   const int64_t col0 = u0 * 4;
-  {
-    constexpr int BATCH = 8;
-    const int nc = K * ncol, total = nc + ncol;
-    for (int i0 = tid; i0 < total; i0 += kCt * BATCH) {
-      float v[BATCH];
-#pragma unroll
-      for (int j = 0; j < BATCH; ++j) {
-        const int i = i0 + j * kCt;
-        v[j] = 0.f;
-        if (i < nc) v[j] = __ldg(p.Cp + (int64_t)(i / ncol) * p.Dp + col0 + i % ncol);
-        else if (i < total) v[j] = __ldg(p.bnorm + col0 + (i - nc));
-      }
-#pragma unroll
-      for (int j = 0; j < BATCH; ++j) {
-        const int i = i0 + j * kCt;
-        if (i < nc) Cs[i] = v[j];
-        else if (i < total) bns[i - nc] = v[j];
-      }
-    }
-  }
   float* sw = Sw + (size_t)warp * NB * K;
   for (int i = lane; i < NB * K; i += 32) sw[i] = 0.f;
   cbar();
