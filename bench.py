@@ -548,6 +548,7 @@ def run_ours(args, rank, world, local_rank):
                                      ("all_reduce(N x K scores)" if (args.dshard and xchg is None and world > 1) else
                                       ("in-kernel peer-memory exchange" if xchg is not None else None))),
                       "dshard_exchange": (("kernel" if xchg is not None else "nccl") if args.dshard else None),
+                      "h_bytes_per_step": (2 * int(Hbuf.numel()) * 4 if args.mode in ("unfused", "train") else 0),
                       "l2": "flushed between steps (untimed write of 2x L2 bytes, then a read of another 2x L2 buffer)",
                       "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "warm": warm, "one_shot": one_shot,

@@ -811,7 +811,14 @@ hdc_status_t hdc_similarity_packed(const uint32_t* H, int64_t ldw, int64_t N, in
   if (!aligned(H, 4) || !aligned(C, 4) || !aligned(labels, 4) || !aligned(scores, 4))
     return fail(HDC_ERR_MISALIGNED, "alignment");
   if (N == 0) return HDC_OK;
-  cudaError_t e = launch_packed_similarity(H, ldw, N, D, C, K, labels, scores, (cudaStream_t)stream);
+  // the tensor-core Stage II (the unfused ablation at its own roofline); HDC_PACKED_FFMA
+  // keeps round 1's FFMA kernel for comparison
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = getenv("HDC_PACKED_FFMA")
+                      ? launch_packed_similarity(H, ldw, N, D, C, K, labels, scores, (cudaStream_t)stream)
+                      : launch_packed_similarity_tc(H, ldw, N, D, C, K, labels, scores, sms, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "packed similarity launch");
   return HDC_OK;
 }

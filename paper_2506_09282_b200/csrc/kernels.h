@@ -154,6 +154,9 @@ cudaError_t launch_small_tc(const SmallTcOperands& o, const float* X, int n, flo
 // k_packed.cu: unfused Stage II from bit-packed H (ablation) and class bundling (training)
 cudaError_t launch_packed_similarity(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,
                                      int64_t K, int32_t* labels, float* scores, cudaStream_t st);
+// k_packed_tc.cu: the same on the tensor cores (bf16 +-1 H unpacked in shared memory, C hi + lo)
+cudaError_t launch_packed_similarity_tc(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const float* C,
+                                        int64_t K, int32_t* labels, float* scores, int num_sms, cudaStream_t st);
 cudaError_t launch_bundle(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const int32_t* y, int64_t K,
                           int32_t* counts, float* M, unsigned* err, cudaStream_t st);
 
