@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default): the config's N split over the ranks + label all-gather "
                          "in the step; weak: every rank infers a whole batch, no collective")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)   # gloo + --same-device: exercise the N>1 code path on one GPU
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-peaks", action="store_true", help="skip the in-run cuBLAS peak probes")
@@ -563,6 +566,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -572,7 +577,10 @@ def main():
         os.environ.setdefault("NCCL_DEBUG", "INFO")         # communicator lines show the rank count
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
