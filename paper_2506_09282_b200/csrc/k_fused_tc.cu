@@ -1354,7 +1354,12 @@ cudaError_t launch_cluster_k(int cl_n, int cl_d, int virt, const CUtensorMap& a,
 // int8 mode: 128-byte K stages when Fp is a multiple of 128 (half the producer / MMA
 // hand-offs), else 64-byte stages (a 128-byte last stage would load 64 bytes of zeros
 // per row: cfg4, F = 784, ran 7% slower)
-int tc_kbytes(int mode, int64_t Fp) { return mode == 2 ? ((Fp % 128 == 0) ? 128 : 64) : HDC_TC_KB16; }
+int tc_kbytes(int mode, int64_t Fp) {
+  if (mode != 2) return HDC_TC_KB16;
+  const char* e = getenv("HDC_TC_KB8");              // measurements: force 64-byte int8 stages
+  if (e && atoi(e) == 64) return 64;
+  return (Fp % 128 == 0) ? 128 : 64;
+}
 template <int MODE, int BN, bool ENC>
 cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
                              const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
