@@ -42,7 +42,10 @@ using namespace ptx;
 constexpr int kCw = HDC_SMALL_CW;              // consumer warps
 constexpr int kCt = 32 * kCw;                  // consumer threads
 constexpr int kThreadsS = kCt + 32;            // + producer warp (lane w feeds consumer warp w)
-constexpr int kChunkRows = 256;                // B4 rows per ring stage (4 KB)
+#ifndef HDC_SMALL_CHUNK
+#define HDC_SMALL_CHUNK 256
+#endif
+constexpr int kChunkRows = HDC_SMALL_CHUNK;    // B4 rows per ring stage (4 KB)
 constexpr int kStagesMax = 8;                  // per consumer warp
 constexpr int kGroup = 8;                      // first-level reduction group (CTAs)
 
