@@ -440,6 +440,28 @@ def run_ours(args, rank, world, local_rank):
     kernel_ms = sum(kms) / len(kms)
     kernel = model.last_kernel()
 
+    # small batches: the attainable one-shot stream of the same bytes under the same flush
+    # protocol (a pure bulk-copy read of the algorithmic bytes, CUDA events), so
+    # the HBM fraction can be read against what a single cold read of that size reaches
+    stream_ceiling = None
+    if n_local <= 32 and world == 1 and args.mode == "infer":
+        nbytes = int(4.0 * cfg.D * (cfg.F + cfg.K) + 4.0 * n_local * cfg.F) // 16 * 16
+        sbuf = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
+        ts = []
+        for i in range(10):
+            flush(i)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            hdc.diag_stream_read(sbuf, nbytes)             # libhdc's one-shot bulk-copy read
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        stream_ceiling = {"us": ts[len(ts) // 2] * 1e3, "gbs": nbytes / (ts[len(ts) // 2] * 1e-3) / 1e9,
+                          "how": "median of 10 one-shot bulk-copy reads of the same byte count "
+                                 "(hdc_diag_stream_read), L2 flushed as for the step"}
+        del sbuf
+
     # small batches: the warm figure -- a CUDA graph of 200 back-to-back
     # calls (no flush, B and C may stay in L2), time / 200
     warm = None
@@ -526,6 +548,9 @@ def run_ours(args, rank, world, local_rank):
     if roof["traffic"] is not None:
         roof["traffic_source"] = "ncu --set full dram bytes per launch (profiles/**/traffic.json)"
     roof["kernel"] = kernel
+    if stream_ceiling is not None and roof["bound"] == "hbm":
+        roof["stream_ceiling"] = stream_ceiling
+        roof["frac_of_stream_ceiling"] = roof["achieved"] / stream_ceiling["gbs"]
     roof["kernel_ms"] = kernel_ms
     roof["kernel_share_of_step"] = kernel_ms / ms_per_step
     cpu = None

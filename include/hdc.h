@@ -242,6 +242,12 @@ const char* hdc_last_error(void);
 /* Library version string. */
 const char* hdc_version(void);
 
+/* Diagnostic (measurement only): read `bytes` bytes of the device buffer `buf` once with
+ * 1-D bulk copies, each SM one contiguous range through an 8 x 16 KB shared-memory ring --
+ * the one-shot streaming ceiling of a read of that size, against which bench.py reads the
+ * small-batch kernels' HBM fraction.  `buf` and `bytes` 16-byte aligned; asynchronous. */
+hdc_status_t hdc_diag_stream_read(const void* buf, int64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

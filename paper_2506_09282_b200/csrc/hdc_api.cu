@@ -502,7 +502,19 @@ const char* hdc_status_string(hdc_status_t st) {
 
 const char* hdc_last_error(void) { return g_last_error.c_str(); }
 
-const char* hdc_version(void) { return "libhdc 0.1 (sm_100a)"; }
+const char* hdc_version(void) { return "libhdc 0.2 (sm_100a)"; }
+
+hdc_status_t hdc_diag_stream_read(const void* buf, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && !buf)) return fail(HDC_ERR_INVALID_VALUE, "null buffer or bytes < 0");
+  if (!aligned(buf, 16) || bytes % 16) return fail(HDC_ERR_MISALIGNED, "16-byte aligned buffer and size required");
+  if (bytes == 0) return HDC_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = launch_stream_read(buf, bytes, sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stream read launch");
+  return HDC_OK;
+}
 
 hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t D, int64_t K,
                               hdc_precision_t prec, hdc_model_t* out) {

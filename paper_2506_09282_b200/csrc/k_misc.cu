@@ -1,6 +1,7 @@
 // k_misc.cu -- K5 row argmax and the model-setup kernels (padding copies, norms).
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace hdc {
 namespace {
@@ -81,7 +82,52 @@ __global__ void col_norm_kernel(const float* __restrict__ Bp, int64_t F, int64_t
   out[d] = __double2float_ru(__dsqrt_ru(s));
 }
 
+// Diagnostic: read `bytes` once with 1-D bulk copies, each CTA one contiguous range through
+// an 8 x 16 KB ring (the one-shot streaming ceiling the small-batch kernels are compared with).
+__global__ void __launch_bounds__(64, 1) stream_read_kernel(const uint8_t* __restrict__ src, int64_t bytes,
+                                                            unsigned* sink) {
+  constexpr int NST = 8, CH = 16384;
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t full[NST];
+  const int64_t per = (bytes / gridDim.x + 15) / 16 * 16;
+  const int64_t b0 = blockIdx.x * per, b1 = (b0 + per < bytes) ? b0 + per : bytes;
+  const int64_t n = b1 > b0 ? (b1 - b0 + CH - 1) / CH : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned acc = 0;
+  if (threadIdx.x == 0) {
+    for (int64_t k = 0; k < n; ++k) {
+      const int s = (int)(k % NST);
+      if (k >= NST) {
+        ptx::mbar_wait(&full[s], (uint32_t)(((k / NST) - 1) & 1));
+        acc += ring[(size_t)s * CH];
+      }
+      const int64_t o = b0 + k * CH;
+      const uint32_t nb = (uint32_t)((b1 - o) < CH ? ((b1 - o) + 15) / 16 * 16 : CH);
+      ptx::mbar_arrive_expect_tx(&full[s], nb);
+      ptx::bulk_load(ring + (size_t)s * CH, src + o, nb, &full[s]);
+    }
+    for (int64_t k = (n > NST ? n - NST : 0); k < n; ++k) {
+      const int s = (int)(k % NST);
+      ptx::mbar_wait(&full[s], (uint32_t)((k / NST) & 1));
+      acc += ring[(size_t)s * CH];
+    }
+    if (acc == 0xFFFFFFFFu) *sink = acc;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_stream_read(const void* buf, int64_t bytes, int num_sms, cudaStream_t st) {
+  const int smem = 8 * 16384;
+  cudaError_t e = cudaFuncSetAttribute(stream_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  stream_read_kernel<<<num_sms, 64, smem, st>>>(static_cast<const uint8_t*>(buf), bytes, nullptr);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st) {
   if (N <= 0) return cudaSuccess;

@@ -160,6 +160,9 @@ cudaError_t launch_packed_similarity_tc(const uint32_t* H, int64_t ldw, int64_t 
 cudaError_t launch_bundle(const uint32_t* H, int64_t ldw, int64_t N, int64_t D, const int32_t* y, int64_t K,
                           int32_t* counts, float* M, unsigned* err, cudaStream_t st);
 
+// Diagnostic one-shot read of `bytes` (16-byte aligned buffer) with bulk copies.
+cudaError_t launch_stream_read(const void* buf, int64_t bytes, int num_sms, cudaStream_t st);
+
 // K5: labels[r] = lowest-index argmax of S[r, 0:K).
 cudaError_t launch_argmax(const float* S, int64_t N, int64_t K, int32_t* labels, cudaStream_t st);
 

@@ -64,6 +64,8 @@ def lib():
         L.hdc_status_string.restype = ctypes.c_char_p
         L.hdc_last_error.restype = ctypes.c_char_p
         L.hdc_version.restype = ctypes.c_char_p
+        L.hdc_diag_stream_read.argtypes = [P, I64, P]
+        L.hdc_diag_stream_read.restype = I32
         for name in ("hdc_infer", "hdc_model_create", "hdc_model_infer", "hdc_model_infer_path",
                      "hdc_model_infer_host", "hdc_model_partial_scores", "hdc_argmax",
                      "hdc_model_infer_dshard",
@@ -268,6 +270,17 @@ def infer(X, B, C, prec="fp32", return_scores=False, stream=None):
         _check(lib().hdc_infer(_ptr(X), _ptr(B), _ptr(C), N, F, D, K, _ptr(labels), _ptr(scores),
                                PREC[prec], _stream_ptr(stream, X.device)))
     return labels, scores
+
+
+def diag_stream_read(buf, nbytes=None, stream=None):
+    """One-shot bulk-copy read of a CUDA tensor's bytes (measurement diagnostic)."""
+    if not (isinstance(buf, torch.Tensor) and buf.is_cuda and buf.is_contiguous()):
+        raise TypeError("buf must be a contiguous CUDA tensor")
+    n = buf.numel() * buf.element_size() if nbytes is None else int(nbytes)
+    if n > buf.numel() * buf.element_size():
+        raise ValueError("nbytes exceeds the buffer")
+    with torch.cuda.device(buf.device):
+        _check(lib().hdc_diag_stream_read(_ptr(buf), n, _stream_ptr(stream, buf.device)))
 
 
 def dshard_exchange_bytes(N, K, world):
