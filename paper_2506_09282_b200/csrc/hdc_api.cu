@@ -54,6 +54,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 constexpr int64_t kMaxF = int64_t(1) << 20;
 constexpr int kSmallMaxN = 32;
 constexpr int kSmallMaxNLowp = 8;          // bf16 / tf32 models (see run())
+constexpr int64_t kWideMinFp = 2048;       // int8 wide K4 from this padded F (cfg5: 3072)
 constexpr int kSmallTcMinN = 5;            // fp32_tc models: K2t from this many rows (see run())
 constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 
@@ -65,6 +66,7 @@ struct hdc_model_s {
   int num_sms = 148;
   hdc_precision_t prec = HDC_PREC_FP32;
   bool fp32_tc = false;       // HDC_PREC_FP32 served by the sign-exact int8 tensor-core kernels
+  bool tc_wide = false;       // int8 K4 in wide mode (160-column tiles, one accumulator; large F)
   float* Bp = nullptr;
   float* Bt = nullptr;
   float* B4 = nullptr;       // unit-major copy of Bp for the small-batch kernel
@@ -74,6 +76,7 @@ struct hdc_model_s {
   int cl_virt = 0;           // 1: virtual 1 x cl_d CTA groups (large F: L2 working set); 2: CTA pair
   void* Btc = nullptr;       // [NL][Dq][Fp]
   int64_t* coltau = nullptr; // [Dq] (int8 limbs)
+  int32_t* coltau_m = nullptr; // [Dq] K4's coarse column taus (tc_flag_shift)
   void* Cil = nullptr;       // per D-tile Stage II operand (tc_c_tile_bytes each)
   // tensor-core workspace, grown with N
   int64_t tw_rows = 0;
@@ -173,6 +176,7 @@ void free_model_memory(hdc_model_s* m) {
   if (m->ev1) cudaEventDestroy(m->ev1);
   cudaFree(m->Btc);
   cudaFree(m->coltau);
+  cudaFree(m->coltau_m);
   cudaFree(m->Cil);
   cudaFree(m->Atc);
   cudaFree(m->rowtau);
@@ -238,18 +242,18 @@ int tc_mode_of(const hdc_model_s* m) {
   switch (m->prec) {
     case HDC_PREC_BF16: return 0;
     case HDC_PREC_TF32: return 1;
-    case HDC_PREC_FP32_TC: return 2;
-    case HDC_PREC_FP32: return m->fp32_tc ? 2 : -1;
+    case HDC_PREC_FP32_TC: return m->tc_wide ? 3 : 2;
+    case HDC_PREC_FP32: return m->fp32_tc ? (m->tc_wide ? 3 : 2) : -1;
     default: return -1;
   }
 }
-int tc_limbs(int mode) { return mode == 2 ? 3 : 1; }
+int tc_limbs(int mode) { return mode >= 2 ? 3 : 1; }
 size_t tc_esz(int mode) { return mode == 0 ? 2 : mode == 1 ? 4 : 1; }
 
 bool tc_eligible(const hdc_model_s* m) {
   const int mode = tc_mode_of(m);
   if (mode < 0 || m->K > tc_max_k(mode)) return false;
-  if (mode == 2 && m->Fp > tc_max_fp_int8()) return false;
+  if (mode >= 2 && m->Fp > tc_max_fp_int8()) return false;
   return m->Btc != nullptr;
 }
 
@@ -281,7 +285,7 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(long long) * nsl * kTileM * tc_kp(m->K));
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (rows / kTileM));
-  if (e == cudaSuccess && mode == 2) {
+  if (e == cudaSuccess && mode >= 2) {
     // list capacity: ~1/256 of the elements (measured ~1e-4 flagged), at most 4M entries;
     // beyond it the kernel re-evaluates inline (correct, slower)
     const int64_t kp = tc_kp(m->K);
@@ -324,7 +328,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   const int64_t gm = kTileM * cl_n;
   const int64_t Np = (N + gm - 1) / gm * gm;
   cudaError_t e;
-  if (mode == 2)
+  if (mode >= 2)
     e = launch_tc_limbs(X, N, Np, m->F, m->F, m->Fp, (int8_t*)m->Atc, m->rowtau, tc_tau_const(m->F), st);
   else
     e = launch_tc_round(mode, X, N, Np, m->F, m->F, m->Fp, m->Atc, st);
@@ -347,6 +351,8 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.Bt = m->Bt;
   o.rowtau = m->rowtau;
   o.coltau = m->coltau;
+  o.coltau_m = m->coltau_m;
+  o.flag_shift = tc_flag_shift(m->Fp);
   o.S_part = m->S_part_tc;
   o.s_part_slots = m->tw_slots;
   o.shift = m->corr_shift;
@@ -369,7 +375,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
   m->last_launches = 2;
   m->last_kernel = HDC_KERNEL_TC;
-  if (mode == 2) {
+  if (mode >= 2) {
     e = launch_tc_recheck(o, N, S, labels, m->corr_shift, st);
     if (e != cudaSuccess) return cuda_fail(e, "tc recheck launch");
     m->last_launches = 4;
@@ -575,24 +581,35 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   // corrections: 2 D max|C| 2^shift < 2^62
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess) m->corr_shift = tc_corr_shift(m->Cp, K * m->Dp, D);
+  {
+    // int8 wide mode (k_fused_tc.cu, mode 3) for large F, where K4 streams its operands
+    // faster than the double-buffered 80-column tiles can consume them; HDC_TC_WIDE=0/1
+    // overrides (measurements)
+    const char* w = getenv("HDC_TC_WIDE");
+    m->tc_wide = K <= tc_max_k(3) && (w ? atoi(w) != 0 : m->Fp >= kWideMinFp);
+  }
   const int mode = tc_mode_of(m);
   const int64_t tn = tc_tile_n(mode < 0 ? 0 : mode, K);
   tc_cluster_shape(mode < 0 ? 0 : mode, K, F, D, &m->cl_n, &m->cl_d, &m->cl_virt);
   m->Dq = (D + tn * m->cl_d - 1) / (tn * m->cl_d) * (tn * m->cl_d);
-  if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode == 2 && m->Fp > tc_max_fp_int8())) {
+  if (e == cudaSuccess && mode >= 0 && K <= tc_max_k(mode) && !(mode >= 2 && m->Fp > tc_max_fp_int8())) {
     e = cudaMalloc(&m->Btc, tc_esz(mode) * tc_limbs(mode) * m->Dq * m->Fp);
-    if (e == cudaSuccess && mode == 2) e = cudaMalloc((void**)&m->coltau, sizeof(int64_t) * m->Dq);
+    if (e == cudaSuccess && mode >= 2) e = cudaMalloc((void**)&m->coltau, sizeof(int64_t) * m->Dq);
+    if (e == cudaSuccess && mode >= 2) e = cudaMalloc((void**)&m->coltau_m, sizeof(int32_t) * m->Dq);
     if (e == cudaSuccess)
       e = cudaMalloc(&m->Cil, (size_t)tc_c_tile_bytes(mode, K) * (m->Dq / tn));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // Bt must be complete
     if (e == cudaSuccess) {
-      if (mode == 2)
+      if (mode >= 2) {
         e = launch_tc_limbs(m->Bt, D, m->Dq, F, m->Fp, m->Fp, (int8_t*)m->Btc, m->coltau, 0, st0);
-      else
+        if (e == cudaSuccess)
+          e = launch_tc_coltau_m(m->coltau, m->Dq, tc_flag_shift(m->Fp), m->coltau_m, st0);
+      } else {
         e = launch_tc_round(mode, m->Bt, D, m->Dq, F, m->Fp, m->Fp, m->Btc, st0);
+      }
     }
     if (e == cudaSuccess) e = launch_tc_c_tiles(mode, m->Cp, K, D, m->Dp, m->Dq, m->Cil, st0);
-    if (e == cudaSuccess && mode == 2) {
+    if (e == cudaSuccess && mode >= 2) {
       // K2t (small-batch tensor-core kernel) accumulators, zero between launches
       if (e == cudaSuccess) e = cudaMalloc((void**)&m->acc_t, sizeof(unsigned long long) * kSmallMaxN * K);
       if (e == cudaSuccess) e = cudaMemset(m->acc_t, 0, sizeof(unsigned long long) * kSmallMaxN * K);
@@ -889,6 +906,11 @@ int64_t hdc_model_recheck_count(hdc_model_t m) {
 int32_t hdc_model_last_launch_count(hdc_model_t m) { return m ? m->last_launches : -1; }
 
 int32_t hdc_model_last_kernel(hdc_model_t m) { return m ? m->last_kernel : -1; }
+
+int32_t hdc_model_tc_tile_n(hdc_model_t m) {
+  if (!m) return -1;
+  return m->Btc ? tc_tile_n(tc_mode_of(m), m->K) : 0;
+}
 
 hdc_status_t hdc_model_set_kernel_timing(hdc_model_t m, int enable) {
   if (!m) return fail(HDC_ERR_INVALID_VALUE, "null model");

@@ -82,36 +82,45 @@ constexpr int KP_MAX_16 = 64;
 // D-tile width by mode and class count: 160 for bf16/tf32 with K <= 32 (an N=160
 // MMA costs the same cycles as N=80, tools/mma_microbench.cu), else 80
 // (int8: three limb accumulators x 80 columns x 2 buffers fill TMEM).
+// mode 3 = the int8 mode with 160-column tiles made of two 80-column sub-tiles and ONE
+// accumulator buffer ("wide", large F only): each A (X limb) stage feeds twice the MMA work,
+// so the operand stream per MMA cycle falls from 81 to 56 bytes per SM
 __host__ __device__ constexpr int tile_n_for(int mode, int64_t K) {
-  return (mode == 2) ? 80 : (K <= 32 ? 160 : 80);
+  return (mode == 2) ? 80 : (mode == 3) ? 160 : (K <= 32 ? 160 : 80);
 }
 
 template <int MODE, int BN_, int KW = 0>
 struct Cfg {
   static constexpr int BN = BN_;
-  static constexpr int NL = (MODE == 2) ? 3 : 1;
+  static constexpr bool I8 = MODE >= 2;                          // int8x3 limbs (modes 2, 3)
+  static constexpr bool WIDE = MODE == 3;
+  static constexpr int NSUB = WIDE ? 2 : 1;                      // 80-column sub-tiles of a tile
+  static constexpr int SUBN = BN / NSUB;
+  static constexpr int NACC = WIDE ? 1 : 2;                      // Stage I accumulator buffers
+  static constexpr int NCS = WIDE ? 1 : 2;                       // C slots
+  static constexpr int NL = I8 ? 3 : 1;
   static constexpr int ESZ = (MODE == 0) ? 2 : (MODE == 1) ? 4 : 1;
   // K bytes per stage = one swizzle-atom row (HDC_TC_KB8 / HDC_TC_KB16).
-  static constexpr int KBYTES = KW ? KW : (MODE == 2) ? HDC_TC_KB8 : HDC_TC_KB16;
+  static constexpr int KBYTES = KW ? KW : I8 ? HDC_TC_KB8 : HDC_TC_KB16;
   static constexpr int SWZ = (KBYTES == 64) ? 4 : 2;             // descriptor layout type
   static constexpr int SBO = 8 * KBYTES;                         // 8-row core group
   // bf16/tf32: NAT swizzle atoms (K blocks of KBYTES) per stage, each a [rows][KBYTES] tile
-  static constexpr int NAT = (MODE == 2) ? 1 : HDC_TC_NAT16;
+  static constexpr int NAT = I8 ? 1 : HDC_TC_NAT16;
   static constexpr int ATOM_A = BM * KBYTES, ATOM_B = BN * KBYTES;
   static constexpr int A_LIMB_BYTES = NAT * ATOM_A;
   static constexpr int B_LIMB_BYTES = NAT * ATOM_B;
   static constexpr int KA = KBYTES / ESZ;                        // K elements per atom
   static constexpr int KE = NAT * KA;                            // K elements per stage
-  static constexpr int KP_MAX = (MODE == 2 || BN > 80) ? KP_MAX_I8 : KP_MAX_16;
+  static constexpr int KP_MAX = WIDE ? 16 : (I8 || BN > 80) ? KP_MAX_I8 : KP_MAX_16;
   // TMEM columns: two Stage I accumulator buffers, the Stage II accumulator (hi and lo C
   // parts accumulate into the same Kp columns) and, for bf16/tf32, two H tiles as the
   // Stage II A operand (bf16 pairs, BN/2 columns each).
-  static constexpr int ACC_STRIDE = (MODE == 2) ? 3 * BN : (BN <= 128 ? 128 : BN);
-  static constexpr int D2_COL = 2 * ACC_STRIDE;
-  static constexpr bool H_TMEM = (MODE != 2);
+  static constexpr int ACC_STRIDE = I8 ? 3 * BN : (BN <= 128 ? 128 : BN);
+  static constexpr int D2_COL = NACC * ACC_STRIDE;
+  static constexpr bool H_TMEM = !I8;
   static constexpr int S_COLS = KP_MAX;
   static constexpr int H_COL = D2_COL + S_COLS;
-  static constexpr int NH = 2;                                    // H tile buffers
+  static constexpr int NH = WIDE ? 1 : 2;                         // H tile buffers
   static_assert(H_COL + (H_TMEM ? NH * BN / 2 : 0) <= 512, "TMEM budget");
   static constexpr int H_BYTES = BM * BN * 2;                    // int8 mode: bf16 H tile in smem
   static constexpr int CORE_SBO = (BN / 8) * 128;                // 8-row groups of core matrices
@@ -119,22 +128,22 @@ struct Cfg {
   static constexpr int CH = (EPI_COLS % 16 == 0) ? 16 : 8;       // columns per TMEM load
   static constexpr int NWB = (EPI_COLS + 31) / 32;               // bit words per thread
   // Stage II operand per D-tile: bf16 hi/lo [2][Kp][BN] interleaved; int8 mode appends the
-  // int64 column taus of the tile.
-  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + (MODE == 2 ? BN * 8 : 0);
+  // tile's coarse int32 column taus (coltau_m).
+  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + (I8 ? BN * 4 : 0);
   static constexpr int H_REGION = H_TMEM ? 0 : NH * H_BYTES;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
-  static constexpr int FIXED = H_REGION + 2 * C_SLOT + 512 + 1024 + 16 + XCHG_BYTES;
+  static constexpr int FIXED = H_REGION + NCS * C_SLOT + 512 + 1024 + 16 + XCHG_BYTES;
   static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / (A_STAGE + B_STAGE);
   static constexpr int STAGES_ = STAGES_FIT < STAGES_MAX ? STAGES_FIT : STAGES_MAX;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES_ * A_STAGE;
   static constexpr int OFF_H = OFF_B + STAGES_ * B_STAGE;
   static constexpr int OFF_C = OFF_H + H_REGION;
-  static constexpr int OFF_X = (OFF_C + 2 * C_SLOT + 15) / 16 * 16;   // argmax exchange [BM] x (value, index)
+  static constexpr int OFF_X = (OFF_C + NCS * C_SLOT + 15) / 16 * 16;   // argmax exchange [BM] x (value, index)
   static constexpr int OFF_BAR = OFF_X + XCHG_BYTES;
   static constexpr int TOTAL = OFF_BAR + 512;
-  static_assert(STAGES_ >= ((KBYTES == 128 && MODE == 2) || NAT > 1 ? 2 : 3), "pipeline depth");
+  static_assert(STAGES_ >= ((KBYTES == 128 && I8) || NAT > 1 ? 2 : 3), "pipeline depth");
   static_assert(OFF_B % 1024 == 0 && OFF_H % 1024 == 0 && OFF_C % 1024 == 0, "alignment");
   static_assert(C_SLOT % 16 == 0, "bulk-copy granule");
   static_assert(TOTAL + 1024 <= 227 * 1024, "shared memory budget");
@@ -149,6 +158,8 @@ struct TcParams {
   const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
   const int64_t* rowtau;   // int8 mode: per-row part of tau (units of 2^14)
   const int64_t* coltau;   // int8 mode: per-column part of tau
+  const int32_t* coltau_m; // int8 mode: ceil(coltau / 2^flag_shift), the epilogue's coarse column taus
+  int flag_shift;          // int8 mode: the epilogue flags on floor(I / 2^flag_shift) (tc_flag_shift)
   const uint8_t* Cil;      // per D-tile Stage II operand (see Cfg::C_SLOT), c_tile_bytes each
   uint32_t c_tile_bytes;
   long long* S_part;       // [CTAs][nslot][BM][Kp] int64 fixed-point partial scores of split N-tiles
@@ -258,7 +269,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // its own shared memory, so each SM ingests 128 + BN/2 operand rows per k-step instead of
   // 128 + BN).  The leader (rank 0) issues every MMA; the peer's epilogue signals the
   // leader's barriers remotely.
-  static_assert(!PAIR || (CLN == 2 && CLD == 1 && HWC && MODE != 2 && !ENC), "pair mode: bf16/tf32 inference, 2x1 cluster");
+  static_assert(!PAIR || (CLN == 2 && CLD == 1 && HWC && !CF::I8 && !ENC), "pair mode: bf16/tf32 inference, 2x1 cluster");
+  constexpr bool I8 = CF::I8;
+  constexpr int KIND = I8 ? 2 : MODE;                // tcgen05 kind: 0 f16, 1 tf32, 2 i8
+  constexpr int NSUB = CF::NSUB, SUBN = CF::SUBN;
+  constexpr int NACC = CF::NACC, NCS = CF::NCS;
   constexpr int NL = CF::NL;
   constexpr int KE = CF::KE;
   constexpr int NH = CF::NH;
@@ -266,9 +281,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   constexpr int CH = CF::CH;
   constexpr int NWB = CF::NWB;
   constexpr int CORE_SBO = CF::CORE_SBO;
-  constexpr uint32_t IDESC = make_idesc<MODE>(BM, BN);
-  constexpr uint32_t IDESC_N160 = make_idesc<MODE>(BM, 2 * BN);
-  constexpr uint32_t IDESC_N240 = make_idesc<MODE>(BM, 3 * BN);
+  constexpr uint32_t IDESC = make_idesc<KIND>(BM, SUBN);
+  constexpr uint32_t IDESC_N160 = make_idesc<KIND>(BM, 2 * SUBN);
+  constexpr uint32_t IDESC_N240 = make_idesc<KIND>(BM, 3 * SUBN);
   constexpr uint32_t STAGE_TX = NL * (CF::A_LIMB_BYTES + CF::B_LIMB_BYTES);
   constexpr int A_LIMB_BYTES = CF::A_LIMB_BYTES;
   constexpr int KBYTES = CF::KBYTES;
@@ -342,7 +357,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, PAIR ? 2 * NUM_EPI : NUM_EPI);   // pair: both CTAs' epilogues
       mbar_init(cfull + b, 1);
-      mbar_init(cempty + b, (MODE == 2 && ENC) ? NUM_EPI : 1);   // encode: epilogue frees taus
+      mbar_init(cempty + b, (I8 && ENC) ? NUM_EPI : 1);   // encode: epilogue frees taus
       mbar_init(hfull + b, PAIR ? 2 * NUM_EPI : NUM_EPI);
       mbar_init(hempty + b, 1);
     }
@@ -369,7 +384,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      constexpr int AR = MC ? BM / CLD : BM, BR = MC ? BN / CLN : BN;   // rows this CTA loads
+      constexpr int AR = MC ? BM / CLD : BM, BR = MC ? SUBN / CLN : SUBN;   // rows this CTA loads
       const int ra = MC ? rd : 0, rb = MC ? rn : 0;       // its slice of the A / B tile
       for (int64_t t = t0; t < t1; ++t) {
         const int ni = (int)(t / p.TdG) * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
@@ -403,13 +418,18 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               for (int a = 0; a < CF::NAT; ++a) {
               uint8_t* da = sA + stage * CF::A_STAGE + l * A_LIMB_BYTES + a * CF::ATOM_A + ra * AR * KBYTES;
               const int ya = (int)(l * p.Np + (int64_t)ni * BM + ra * AR);
-              uint8_t* db = sB + stage * CF::B_STAGE + l * CF::B_LIMB_BYTES + a * CF::ATOM_B + rb * BR * KBYTES;
-              const int yb = (int)(l * p.Dq + (int64_t)di * BN + rb * BR);
               const int xk = kb * KE + a * CF::KA;
               if constexpr (MC && CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, xk, ya, a_mask);
               else tma_load_2d(da, &tmA, full + stage, xk, ya);
-              if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, xk, yb, b_mask);
-              else tma_load_2d(db, &tmB, full + stage, xk, yb);
+              // B stage layout [sub-tile][limb][SUBN rows]: each sub-tile's [b0; b1; b2] contiguous
+#pragma unroll
+              for (int h = 0; h < NSUB; ++h) {
+                uint8_t* db = sB + stage * CF::B_STAGE + (h * NL + l) * (CF::B_LIMB_BYTES / NSUB) +
+                              a * CF::ATOM_B + rb * BR * KBYTES;
+                const int yb = (int)(l * p.Dq + (int64_t)di * BN + h * SUBN + rb * BR);
+                if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, xk, yb, b_mask);
+                else tma_load_2d(db, &tmB, full + stage, xk, yb);
+              }
             }
             }
           }
@@ -422,7 +442,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   } else if (warp == 1 && leader) {
     // ===================================================== Stage I MMA issuer (elected lane)
-    constexpr uint32_t IDESC_P = make_idesc<MODE>(2 * BM, BN);   // pair: M = 256
+    constexpr uint32_t IDESC_P = make_idesc<KIND>(2 * BM, BN);   // pair: M = 256
     int stage = 0, buf = 0;
     uint32_t phase = 0, bphase = 0;
     const uint64_t a_desc0 = sdesc(smem_u32(sA));
@@ -444,18 +464,22 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint64_t b_d = b_desc0 + (uint64_t)((stage * CF::B_STAGE) >> 4);
         if (!(DBG(1))) {
           const uint32_t acc = (kb == 0) ? 0u : 1u;
-          if constexpr (MODE == 2) {
+          if constexpr (I8) {
             // The three B limb tiles are contiguous rows [b0; b1; b2] (240 x 64 B) and
             // the accumulators contiguous columns [A0 | A1 | A2], so one MMA per A limb:
             //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
             // (each A tile is read from shared memory once per k-step, not 3 times).
+            // Wide mode: the same for each 80-column sub-tile h, accumulators at 240 h.
             const int nks = (kb == KB - 1) ? last_ks : KBYTES / 32;
 #pragma unroll
             for (int ks = 0; ks < KBYTES / 32; ++ks)
               if (ks < nks)
-              tc_mma_i8x3_elect(acc0, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
-                                a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
-                                IDESC_N160, IDESC, BN, ks == 0 ? acc : 1u);
+#pragma unroll
+                for (int h = 0; h < NSUB; ++h)
+                  tc_mma_i8x3_elect(acc0 + h * 3 * SUBN, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
+                                    a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4),
+                                    b_d + ((h * 3 * SUBN * KBYTES) >> 4) + 2 * ks, IDESC_N240, IDESC_N160,
+                                    IDESC, SUBN, ks == 0 ? acc : 1u);
           } else {
             const int nat = (kb == KB - 1) ? last_at : CF::NAT;
 #pragma unroll
@@ -489,11 +513,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       if constexpr (PAIR) tc_commit_pair_mc_elect(tfull + buf, (uint16_t)3);
       else tc_commit_elect(tfull + buf);
-      buf ^= 1;
-      if (buf == 0) bphase ^= 1;
+      if (++buf == NACC) {
+        buf = 0;
+        bphase ^= 1;
+      }
     }
   } else if (warp == 2) {
-    if ((!ENC || MODE == 2) && !(DBG(8192))) {   // encode mode: only the int8 column taus
+    if ((!ENC || I8) && !(DBG(8192))) {   // encode mode: only the int8 column taus
     // ===================================================== C-tile producer (Stage II B operand)
     // A separate warp, so the operand stream never waits for a C slot.
     if (lane == 0) {
@@ -516,14 +542,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (cs == 0) cphase ^= 1;
           continue;
         }
-        mbar_arrive_expect_tx(cfull + cs, (ENC ? 0u : c_tile_bytes) + (MODE == 2 ? BN * 8 : 0));
+        mbar_arrive_expect_tx(cfull + cs, (ENC ? 0u : c_tile_bytes) + (I8 ? BN * 4 : 0));
         if (!ENC)
           bulk_load(sC + cs * CF::C_SLOT, p.Cil + (int64_t)di * c_tile_bytes, c_tile_bytes, cfull + cs);
-        if constexpr (MODE == 2)
-          bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau + (int64_t)di * BN, BN * 8,
+        if constexpr (I8)
+          bulk_load(sC + cs * CF::C_SLOT + c_tile_bytes, p.coltau_m + (int64_t)di * BN, BN * 4,
                     cfull + cs);
-        cs ^= 1;
-        if (cs == 0) cphase ^= 1;
+        if (++cs == NCS) {
+          cs = 0;
+          cphase ^= 1;
+        }
       }
     }
     }
@@ -582,8 +610,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         hb = 0;
         hphase ^= 1;
       }
-      cs ^= 1;
-      if (cs == 0) cphase ^= 1;
+      if (++cs == NCS) {
+        cs = 0;
+        cphase ^= 1;
+      }
     }
     }
   } else if (warp >= EPI_WARP0 && !(DBG(8192))) {
@@ -651,13 +681,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       if (cq == 0 && row >= 0 && p.labels) p.labels[row] = best;
     };
     int64_t next_drain = t0;                          // next tile whose S(t) is to be added
+    const int fsl = 14 - p.flag_shift, fs1 = p.flag_shift - 7, fs2 = p.flag_shift;   // int8 flag test
     for (int64_t t = t0; t < t1; ++t) {
       const int ng = (int)(t / p.TdG);
       const int ni = ng * CLN + rn, di = (int)(t % p.TdG) * CLD + rd;
       const int64_t row = (int64_t)ni * BM + m;
       const bool row_ok = row < p.N;
-      int64_t rtau = -1;                    // int8 mode: row part of tau
-      if constexpr (MODE == 2) rtau = row_ok ? __ldg(p.rowtau + row) : -(int64_t(1) << 62);
+      // int8 mode: row part of the coarse tau, ceil(rowtau / 2^flag_shift); padding rows never flag
+      int32_t mrow = -(1 << 28);
+      if constexpr (I8)
+        if (row_ok) mrow = (int32_t)((__ldg(p.rowtau + row) + (int64_t(1) << p.flag_shift) - 1) >> p.flag_shift);
       if (DBG(256)) {                  // diagnostics: sleep-polling instead of try_wait
         while (!mbar_test(tfull + buf, bphase)) __nanosleep(500);
       }
@@ -669,43 +702,65 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           drain_s();
           ++next_drain;
         }
-      const int64_t* sct = nullptr;         // column taus of this tile (int8 mode), in smem
-      if constexpr (MODE == 2) {
+      const int32_t* scm = nullptr;         // coarse column taus of this tile (int8 mode), in smem
+      if constexpr (I8) {
         TWAIT(15, cfull + cs, cphase);
-        sct = reinterpret_cast<const int64_t*>(sC + cs * CF::C_SLOT + c_tile_bytes);
+        scm = reinterpret_cast<const int32_t*>(sC + cs * CF::C_SLOT + c_tile_bytes) + cq * EPI_COLS;
+        static_assert((EPI_COLS * 4) % 16 == 0, "16-byte column-tau loads");
       }
       tc_fence_after();
       // ---- phase 1: accumulator -> HardSign bits (bit set -> h = -1) and recheck flags
       uint32_t hbits[NWB], flags[NWB];
 #pragma unroll
       for (int w = 0; w < NWB; ++w) hbits[w] = flags[w] = 0u;
-      const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE + cq * EPI_COLS;
-      if constexpr (MODE == 2) {
-        // 64-bit masks (EPI_COLS <= 64): register-resident under any unrolling
-        static_assert(EPI_COLS <= 64, "int8 column group");
-        uint64_t hb64 = 0, fl64 = 0;
+      // int8: limb accumulators A0 | A1 | A2 of SUBN columns each; wide mode: column group cq
+      // is sub-tile cq (its three accumulators at 3 SUBN cq)
+      const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE +
+                             (CF::WIDE ? cq * 3 * SUBN : cq * EPI_COLS);
+      if constexpr (I8) {
+        // 64-bit masks (two for EPI_COLS = 80): register-resident under any unrolling
+        static_assert(EPI_COLS <= 128, "int8 column group");
+        uint64_t hb64 = 0, fl64 = 0, hb64x = 0, fl64x = 0;
 #pragma unroll kI8EpiUnroll
         for (int ch = 0; ch < ((DBG(16)) ? 0 : EPI_COLS / CH); ++ch) {
           const int cl = ch * CH;             // column within this thread's group
           uint32_t r0[CH], r1[CH], r2[CH];
           if constexpr (CH == 16) {
             tmem_ld16(tbase + cl, r0);
-            tmem_ld16(tbase + BN + cl, r1);
-            tmem_ld16(tbase + 2 * BN + cl, r2);
+            tmem_ld16(tbase + SUBN + cl, r1);
+            tmem_ld16(tbase + 2 * SUBN + cl, r2);
           } else {
             tmem_ld8(tbase + cl, r0);
-            tmem_ld8(tbase + BN + cl, r1);
-            tmem_ld8(tbase + 2 * BN + cl, r2);
+            tmem_ld8(tbase + SUBN + cl, r1);
+            tmem_ld8(tbase + 2 * SUBN + cl, r2);
           }
           tmem_ld_wait();
+          uint32_t hc = 0, fc = 0;            // this chunk's bits
+          int32_t mc[CH];
+#pragma unroll
+          for (int v = 0; v < CH / 4; ++v) {
+            const int4 q4 = reinterpret_cast<const int4*>(scm + cl)[v];
+            mc[4 * v] = q4.x; mc[4 * v + 1] = q4.y; mc[4 * v + 2] = q4.z; mc[4 * v + 3] = q4.w;
+          }
 #pragma unroll
           for (int j = 0; j < CH; ++j) {
-            const int64_t I = (int64_t)(int32_t)r0[j] * 16384 + (int64_t)(int32_t)r1[j] * 128 +
-                              (int64_t)(int32_t)r2[j];
-            const int b = cl + j;
-            const int64_t aI = I < 0 ? -I : I;
-            hb64 |= (uint64_t)(I < 0) << b;
-            fl64 |= (uint64_t)(aI <= rtau + sct[cq * EPI_COLS + b]) << b;   // tau = -inf past D
+            // I = r0 2^14 + r1 2^7 + r2 (exact, 64-bit) is only needed through
+            // J = r0 2^(14-s) + floor(r1 / 2^(s-7)) + floor(r2 / 2^s), 7 <= s <= 14
+            // (tc_flag_shift), which is floor(I / 2^s) or one less, |J| < 2^31.  With
+            // J' = (J >= 0 ? J : -J - 1): |I| <= tau implies J' <= mrow + mcol (the ceilings
+            // of tau's parts / 2^s), so every element of |I| <= tau is flagged;
+            // an unflagged element has J' > mrow + mcol >= 2, where sign(J) = sign(I).
+            const int32_t J = ((int32_t)r0[j] << fsl) + ((int32_t)r1[j] >> fs1) + ((int32_t)r2[j] >> fs2);
+            const int32_t sg = J >> 31;
+            hc |= (uint32_t)sg & (1u << j);
+            if ((J ^ sg) - mc[j] <= mrow) fc |= 1u << j;   // past D: mcol = -2^28, never
+          }
+          if (EPI_COLS <= 64 || cl < 64) {
+            hb64 |= (uint64_t)hc << cl;
+            fl64 |= (uint64_t)fc << cl;
+          } else {
+            hb64x |= (uint64_t)hc << (cl - 64);
+            fl64x |= (uint64_t)fc << (cl - 64);
           }
         }
         hbits[0] = (uint32_t)hb64;
@@ -713,6 +768,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if constexpr (NWB > 1) {
           hbits[1] = (uint32_t)(hb64 >> 32);
           flags[1] = (uint32_t)(fl64 >> 32);
+        }
+        if constexpr (NWB > 2) {
+          hbits[2] = (uint32_t)hb64x;
+          flags[2] = (uint32_t)fl64x;
         }
       } else {
 #pragma unroll
@@ -733,7 +792,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       __syncwarp();
       if (lane == 0) {
         arrive_lead(tempty + buf);                // accumulator free for tile t + 2
-        if (MODE == 2 && ENC) mbar_arrive(cempty + cs);   // encode mode: taus read
+        if (I8 && ENC) mbar_arrive(cempty + cs);   // encode mode: taus read
       }
       // H buffer hb free (Stage II of tile t - 2 done)
       if constexpr (!ENC) {
@@ -744,7 +803,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // provisional sign used in H; hdc_recheck_kernel re-evaluates them in float64 after
       // this kernel and corrects S exactly where a sign flips (Stage II is linear in H).
       // Only a list overflow (e.g. many all-zero rows) falls back to re-evaluating here.
-      if constexpr (MODE == 2) {
+      if constexpr (I8) {
 #pragma unroll
         for (int w = 0; w < NWB; ++w) {
           uint32_t fw = (DBG(512)) ? 0u : flags[w];   // 512: diagnostics, no rechecks
@@ -845,14 +904,18 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0 && !ENC) arrive_lead(hfull + hb);
-      buf ^= 1;
-      if (buf == 0) bphase ^= 1;
+      if (++buf == NACC) {
+        buf = 0;
+        bphase ^= 1;
+      }
       if (++hb == NH) {
         hb = 0;
         hphase ^= 1;
       }
-      cs ^= 1;
-      if (cs == 0) cphase ^= 1;
+      if (++cs == NCS) {
+        cs = 0;
+        cphase ^= 1;
+      }
 
       // ---- end of this CTA's run of D-tiles for N-tile ni: the last two tiles' S as well
       if (ENC || !seg_last(t, t1, p.TdG)) continue;
@@ -980,7 +1043,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       named_bar(1, NUM_EPI * 32);     // s_flag reuse
     }
-    if (MODE == 2 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
+    if (I8 && lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
   if ((DBG(4)) && lane == 0 && (warp <= 3 || warp == EPI_WARP0)) {
     if (warp != EPI_WARP0) dbgc[15] = 0;
@@ -1335,7 +1398,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
 template <int MODE, int BN, bool ENC, int KW>
 cudaError_t launch_cluster_k(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
                              const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
-  if constexpr (MODE != 2 && !ENC) {
+  if constexpr (MODE < 2 && !ENC) {
     if (virt == 2 && cl_n == 2 && cl_d == 1)   // CTA pair as one cta_group::2 MMA unit
       return launch_mode<MODE, BN, 2, 1, false, true, true>(a, b, c, p, num_sms, st);
   }
@@ -1355,6 +1418,7 @@ cudaError_t launch_cluster_k(int cl_n, int cl_d, int virt, const CUtensorMap& a,
 // hand-offs), else 64-byte stages (a 128-byte last stage would load 64 bytes of zeros
 // per row: cfg4, F = 784, ran 7% slower)
 int tc_kbytes(int mode, int64_t Fp) {
+  if (mode == 3) return 64;                            // wide: 3 stages of 54 KB
   if (mode != 2) return HDC_TC_KB16;
   const char* e = getenv("HDC_TC_KB8");              // measurements: force 64-byte int8 stages
   if (e && atoi(e) == 64) return 64;
@@ -1363,7 +1427,9 @@ int tc_kbytes(int mode, int64_t Fp) {
 template <int MODE, int BN, bool ENC>
 cudaError_t launch_cluster_e(int cl_n, int cl_d, int virt, const CUtensorMap& a, const CUtensorMap& b,
                              const CUtensorMap& c, TcParams& p, int num_sms, cudaStream_t st) {
-  if constexpr (MODE == 2) {
+  if constexpr (MODE == 3) {
+    return launch_cluster_k<MODE, BN, ENC, 64>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
+  } else if constexpr (MODE == 2) {
     if (tc_kbytes(MODE, p.Fp) == 128)
       return launch_cluster_k<MODE, BN, ENC, 128>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
     return launch_cluster_k<MODE, BN, ENC, 64>(cl_n, cl_d, virt, a, b, c, p, num_sms, st);
@@ -1406,9 +1472,9 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   // DRAM per launch), a virtual 1 x g group puts g CTAs on each N-tile (g = 4, 8, 16).
   const int bn = tile_n_for(mode, K);
   int n = 2, d = 1, v = 0;
-  if (bn == 80 && mode != 2) n = 1;               // (bf16/tf32 with K > 32: no cluster)
+  if (bn == 80 && mode < 2) n = 1;                // (bf16/tf32 with K > 32: no cluster)
   const int64_t Fp = (F + 63) / 64 * 64;
-  const double esz_nl = (mode == 2) ? 3.0 : (mode == 0 ? 2.0 : 4.0);
+  const double esz_nl = (mode >= 2) ? 3.0 : (mode == 0 ? 2.0 : 4.0);
   const double a_tile = 128.0 * Fp * esz_nl, b_all = (double)(D + bn) * Fp * esz_nl;
   const double l2 = 120e6;                        // of the 126 MB L2, leaving room for C, S
   if (148.0 * a_tile + b_all > l2) {
@@ -1424,10 +1490,10 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   char vc = 0;
   if (env) {
     const int got = sscanf(env, "%dx%d%c", &en, &ed, &vc);
-    if (got >= 2 && !(bn == 80 && mode != 2)) {
+    if (got >= 2 && !(bn == 80 && mode < 2)) {
       if (got == 3 && vc == 'v' && en == 1 && (ed == 4 || ed == 8 || ed == 16)) {
         n = 1; d = ed; v = 1;
-      } else if (got == 3 && vc == 'p' && en == 2 && ed == 1) {
+      } else if (got == 3 && vc == 'p' && en == 2 && ed == 1 && mode < 2) {
         n = 2; d = 1; v = 2;                      // CTA pair (cta_group::2)
       } else if (got == 2 && ((en == 1 && (ed == 1 || ed == 2)) || (en == 2 && ed == 1))) {
         n = en; d = ed; v = 0;
@@ -1438,13 +1504,36 @@ void tc_cluster_shape(int mode, int64_t K, int64_t F, int64_t D, int* cl_n, int*
   *cl_d = d;
   *virt = v;
 }
-int tc_max_k(int mode) { return mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
+int tc_max_k(int mode) { return mode == 3 ? 16 : mode == 2 ? KP_MAX_I8 : KP_MAX_16; }
 int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
 int64_t tc_c_tile_bytes(int mode, int64_t K) {
   const int64_t bn = tile_n_for(mode, K);
   return 2 * tc_kp(K) * bn * 2;            // bf16 hi + lo, [Kp][bn] each
 }
 int64_t tc_max_fp_int8() { return 100000; }
+
+// Shift of the epilogue's coarse flag test: |I| < 2^28.03 Fp (three int8 limb products per
+// element), so floor(I / 2^s) with 2^s >= Fp / 2 fits in 30 bits; the granularity 2^s is
+// at most ~3% of the smallest tau (>= 64 F), so the coarse test flags few extra elements.
+int tc_flag_shift(int64_t Fp) {
+  int s = 0;
+  while ((int64_t(1) << (s + 1)) < Fp) ++s;          // 2^(s+1) >= Fp
+  // 7 <= s <= 14 for the 32-bit form of the test (at Fp <= tc_max_fp_int8, |J| < 2^30.7)
+  return s < 7 ? 7 : s > 14 ? 14 : s;
+}
+
+__global__ void coltau_m_kernel(const int64_t* __restrict__ coltau, int64_t Dq, int shift, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Dq) return;
+  const int64_t t = coltau[i];
+  // ceil(t / 2^shift); columns past D (t = -2^62) never flag
+  out[i] = t < 0 ? -(1 << 28) : (int32_t)((t + (int64_t(1) << shift) - 1) >> shift);
+}
+
+cudaError_t launch_tc_coltau_m(const int64_t* coltau, int64_t Dq, int shift, int32_t* out, cudaStream_t st) {
+  coltau_m_kernel<<<(unsigned)((Dq + 255) / 256), 256, 0, st>>>(coltau, Dq, shift, out);
+  return cudaGetLastError();
+}
 
 int64_t tc_tau_const(int64_t F) {
   // F (0.390625 + 2^20 + 2^12) + 1, in the integer units of U_x.U_b (before the 2^-14 scale)
@@ -1553,6 +1642,8 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.Bt = o.Bt;
   p.rowtau = o.rowtau;
   p.coltau = o.coltau;
+  p.coltau_m = o.coltau_m;
+  p.flag_shift = o.flag_shift;
   p.Cil = (const uint8_t*)o.Cil;
   p.c_tile_bytes = (uint32_t)tc_c_tile_bytes(mode, o.K);
   p.S_part = o.S_part;
@@ -1586,7 +1677,8 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
     memset(wd_host, 0, (8 + 4 * 64) * sizeof(unsigned long long));
     cudaHostGetDevicePointer((void**)&p.dbg, wd_host, 0);
   }
-  const int nl = (mode == 2) ? 3 : 1;
+  const int nl = (mode >= 2) ? 3 : 1;
+  const int subn = (mode == 3) ? bn / 2 : bn;  // wide: B loads per 80-column sub-tile
   const int esz = (mode == 0) ? 2 : (mode == 1) ? 4 : 1;
   const CUtensorMapDataType dt = (mode == 0)   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : (mode == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
@@ -1595,7 +1687,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   const uint32_t kbytes = (uint32_t)tc_kbytes(mode, o.Fp);
   const CUtensorMapSwizzle swz = (kbytes == 64) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   // boxes: this CTA's slice of the tile (the rest arrives by multicast from cluster peers)
-  const int a_rows = o.cl_virt == 1 ? BM : BM / o.cl_d, b_rows = o.cl_virt == 1 ? bn : bn / o.cl_n;
+  const int a_rows = o.cl_virt == 1 ? BM : BM / o.cl_d, b_rows = o.cl_virt == 1 ? subn : subn / o.cl_n;
   if (!make_map_2d(&ma, dt, esz, o.A, (uint64_t)o.Fp, (uint64_t)nl * o.N_p, kbytes / esz, a_rows, swz) ||
       !make_map_2d(&mb, dt, esz, o.B, (uint64_t)o.Fp, (uint64_t)nl * o.Dq, kbytes / esz, b_rows, swz))
     return cudaErrorInvalidValue;
@@ -1610,6 +1702,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   if (mode == 0 && bn == 160) e = launch_cluster<0, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
   else if (mode == 1 && bn == 160) e = launch_cluster<1, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
   else if (mode == 2) e = launch_cluster<2, 80>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
+  else if (mode == 3) e = launch_cluster<3, 160>(o.cl_n, o.cl_d, o.cl_virt, ma, mb, mc, p, num_sms, st);
   else if (o.cl_n == 1 && o.cl_d == 1)
     e = (mode == 0) ? (p.hout ? launch_mode<0, 80, 1, 1, true>(ma, mb, mc, p, num_sms, st)
                               : launch_mode<0, 80, 1, 1, false>(ma, mb, mc, p, num_sms, st))
@@ -1630,7 +1723,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
     unsigned long long h[512];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg_buf + 16, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[hdc tc timeline] CTA 0, KB=%d stages/tile; MMA full-wait exits / producer empty-wait exits (cycles from first):\n", (int)(p.Fp / (mode == 2 ? 64 : (mode == 0 ? 64 : 32))));
+    fprintf(stderr, "[hdc tc timeline] CTA 0, KB=%d stages/tile; MMA full-wait exits / producer empty-wait exits (cycles from first):\n", (int)(p.Fp / (mode >= 2 ? 64 : (mode == 0 ? 64 : 32))));
     for (int i = 0; i < 64; ++i)
       fprintf(stderr, "  stage %3d: mma %8lld  prod %8lld\n", i, (long long)(h[i] - h[0]), (long long)(h[256 + i] - h[0]));
   }

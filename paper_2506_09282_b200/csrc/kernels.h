@@ -74,7 +74,8 @@ cudaError_t launch_prep_x(const float* X, int64_t N, int64_t F, int64_t Fp, floa
 cudaError_t launch_fused_ffma(const ModelView& m, const FusedWorkspace& ws, const float* X, int64_t N,
                               float* scores, int32_t* labels, bool recheck, int R, cudaStream_t st);
 
-// K4: fused tcgen05 kernel.  mode 0 = bf16, 1 = tf32, 2 = int8x3 (sign-exact).
+// K4: fused tcgen05 kernel.  mode 0 = bf16, 1 = tf32, 2 = int8x3 (sign-exact), 3 = int8x3
+// with 160-column tiles (two 80-column sub-tiles, one accumulator buffer; large F).
 struct TcOperands {
   int64_t F, Fp, D, Dp, Dq, K, N_p;  // Dq = D rounded up to cl_d D-tiles; N_p to cl_n x 128 rows
   int cl_n, cl_d;                    // thread-block cluster shape (N-tiles x D-tiles), multicast
@@ -86,6 +87,8 @@ struct TcOperands {
   const float* Bt;                   // [Dp][Fp] fp32 (fp64 recheck)
   const int64_t* rowtau;             // [N_p] int8 mode
   const int64_t* coltau;             // [Dq]  int8 mode
+  const int32_t* coltau_m;           // [Dq]  int8 mode: ceil(coltau / 2^flag_shift) (tc_flag_shift)
+  int flag_shift;
   long long* S_part;                 // [s_part_slots][128][Kp] int64 fixed-point partial scores
   int64_t s_part_slots;
   int shift;                         // fixed-point shift of the Stage II sums (tc_corr_shift)
@@ -113,6 +116,8 @@ cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, i
                               void* out, cudaStream_t st);
 int64_t tc_max_fp_int8();
 int64_t tc_tau_const(int64_t F);
+int tc_flag_shift(int64_t Fp);
+cudaError_t launch_tc_coltau_m(const int64_t* coltau, int64_t Dq, int shift, int32_t* out, cudaStream_t st);
 cudaError_t launch_tc_limbs(const float* src, int64_t rows, int64_t rows_p, int64_t F, int64_t ld_src,
                             int64_t Fp, int8_t* out, int64_t* tau_part, int64_t tau_const,
                             cudaStream_t st);

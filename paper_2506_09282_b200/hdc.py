@@ -56,6 +56,8 @@ def lib():
         L.hdc_model_last_launch_count.restype = ctypes.c_int32
         L.hdc_model_last_kernel.argtypes = [P]
         L.hdc_model_last_kernel.restype = ctypes.c_int32
+        L.hdc_model_tc_tile_n.argtypes = [P]
+        L.hdc_model_tc_tile_n.restype = ctypes.c_int32
         L.hdc_model_set_kernel_timing.argtypes = [P, I32]
         L.hdc_model_set_kernel_timing.restype = I32
         L.hdc_model_last_kernel_ms.argtypes = [P]
@@ -235,6 +237,10 @@ class Model:
     def last_kernel(self):
         """Kernel family of the last call: "none", "small", "ffma" or "tc" (hdc_model_last_kernel)."""
         return KERNELS.get(int(lib().hdc_model_last_kernel(self._h)), "invalid")
+
+    def tc_tile_n(self):
+        """D-tile width of the fused tensor-core kernel (160: int8 wide mode), 0 if none."""
+        return int(lib().hdc_model_tc_tile_n(self._h))
 
     def set_kernel_timing(self, enable=True):
         _check(lib().hdc_model_set_kernel_timing(self._h, 1 if enable else 0))
