@@ -120,16 +120,21 @@ struct Cfg {
   static constexpr bool H_TMEM = !I8;
   static constexpr int S_COLS = KP_MAX;
   static constexpr int H_COL = D2_COL + S_COLS;
-  static constexpr int NH = WIDE ? 1 : 2;                         // H tile buffers
+  // H tile buffers: int8 (H in shared memory) one -- Stage II(t) completes long before the
+  // epilogue writes H(t+1) -- which leaves room for the third C part
+  static constexpr int NH = I8 ? 1 : 2;
+  // C parts of the Stage II operand: bf16 hi + lo (+ a third for the int8 / fp32-semantics
+  // modes, hi + mid + lo = C exactly for normal C)
+  static constexpr int NCP = I8 ? 3 : 2;
   static_assert(H_COL + (H_TMEM ? NH * BN / 2 : 0) <= 512, "TMEM budget");
   static constexpr int H_BYTES = BM * BN * 2;                    // int8 mode: bf16 H tile in smem
   static constexpr int CORE_SBO = (BN / 8) * 128;                // 8-row groups of core matrices
   static constexpr int EPI_COLS = BN / NUM_CQ;                   // columns per epilogue thread
   static constexpr int CH = (EPI_COLS % 16 == 0) ? 16 : 8;       // columns per TMEM load
   static constexpr int NWB = (EPI_COLS + 31) / 32;               // bit words per thread
-  // Stage II operand per D-tile: bf16 hi/lo [2][Kp][BN] interleaved; int8 mode appends the
+  // Stage II operand per D-tile: bf16 parts [NCP][Kp][BN] interleaved; int8 mode appends the
   // tile's coarse int32 column taus (coltau_m).
-  static constexpr int C_SLOT = 2 * KP_MAX * BN * 2 + (I8 ? BN * 4 : 0);
+  static constexpr int C_SLOT = NCP * KP_MAX * BN * 2 + (I8 ? BN * 4 : 0);
   static constexpr int H_REGION = H_TMEM ? 0 : NH * H_BYTES;
   static constexpr int A_STAGE = NL * A_LIMB_BYTES;
   static constexpr int B_STAGE = NL * B_LIMB_BYTES;
@@ -579,7 +584,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       for (int s = 0; s < BN / 16; ++s) {
         const uint32_t acc = (s == 0) ? 0u : 1u;
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {      // C = hi + lo, both into the same columns
+        for (int part = 0; part < (PAIR ? 2 : CF::NCP); ++part) {   // C = hi + lo (+ mid), one accumulator
           const uint64_t bd = smem_desc_interleaved(
               c_base + part * part_bytes + s * 2 * CORE_LBO, CORE_LBO, CORE_SBO);
           if (DBG(8)) continue;
@@ -1222,17 +1227,19 @@ __global__ void round_rows_kernel(const float* __restrict__ src, int64_t rows, i
 }
 
 
-// C tiles for Stage II: per D-tile di, bf16 hi = RN(C), lo = RN(C - hi), each
-// [Kp][bn] in the interleaved K-major core-matrix layout the MMA B descriptor
-// expects (core matrix (g, j) = rows 8g.., columns 8j.. at byte (g bn/8 + j) * 128).
+// C tiles for Stage II: per D-tile di, bf16 hi = RN(C), lo = RN(C - hi) (two parts), or
+// hi, mid = RN(C - hi), lo = RN(C - hi - mid) (three parts: C - hi and C - hi - mid are
+// exact in fp32, and hi + mid + lo = C for normal C), each [Kp][bn] in the interleaved
+// K-major core-matrix layout the MMA B descriptor expects (core matrix (g, j) = rows 8g..,
+// columns 8j.. at byte (g bn/8 + j) * 128).
 __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int64_t Kp, int64_t D,
-                                    int64_t Dp, int64_t Td, int bn, __nv_bfloat16* __restrict__ out) {
+                                    int64_t Dp, int64_t Td, int bn, int nparts, __nv_bfloat16* __restrict__ out) {
   const int64_t per_part = Kp * bn;
-  const int64_t total = Td * 2 * per_part;
+  const int64_t total = Td * nparts * per_part;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t di = i / (2 * per_part);
-    const int part = (int)((i / per_part) % 2);
+    const int64_t di = i / (nparts * per_part);
+    const int part = (int)((i / per_part) % nparts);
     const int64_t e = i % per_part;          // element index inside the interleaved part
     const int64_t core = e / 64, inner = e % 64;
     const int64_t g = core / (bn / 8), j = core % (bn / 8);
@@ -1240,7 +1247,9 @@ __global__ void c_interleave_kernel(const float* __restrict__ Cp, int64_t K, int
     const int64_t d = di * bn + cc;
     const float v = (r < K && d < D) ? Cp[r * Dp + d] : 0.f;
     const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    out[i] = part == 0 ? hi : __float2bfloat16_rn(v - __bfloat162float(hi));
+    const float r1 = v - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    out[i] = part == 0 ? hi : (part == 1 ? mid : __float2bfloat16_rn(r1 - __bfloat162float(mid)));
   }
 }
 
@@ -1508,7 +1517,7 @@ int tc_max_k(int mode) { return mode == 3 ? 16 : mode == 2 ? KP_MAX_I8 : KP_MAX_
 int64_t tc_kp(int64_t K) { return (K + 15) / 16 * 16; }
 int64_t tc_c_tile_bytes(int mode, int64_t K) {
   const int64_t bn = tile_n_for(mode, K);
-  return 2 * tc_kp(K) * bn * 2;            // bf16 hi + lo, [Kp][bn] each
+  return (mode >= 2 ? 3 : 2) * tc_kp(K) * bn * 2;   // bf16 parts (c_interleave_kernel), [Kp][bn] each
 }
 int64_t tc_max_fp_int8() { return 100000; }
 
@@ -1581,10 +1590,11 @@ cudaError_t launch_tc_c_tiles(int mode, const float* Cp, int64_t K, int64_t D, i
   const int bn = tile_n_for(mode, K);
   const int64_t Td = Dq / bn;                 // includes cluster padding tiles (all zero)
   const int64_t Kp = tc_kp(K);
-  const int64_t total = Td * 2 * Kp * bn;
+  const int nparts = mode >= 2 ? 3 : 2;
+  const int64_t total = Td * nparts * Kp * bn;
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 16) grid = 148 * 16;
-  c_interleave_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, Kp, D, Dp, Td, bn, (__nv_bfloat16*)out);
+  c_interleave_kernel<<<(unsigned)grid, 256, 0, st>>>(Cp, K, Kp, D, Dp, Td, bn, nparts, (__nv_bfloat16*)out);
   return cudaGetLastError();
 }
 
