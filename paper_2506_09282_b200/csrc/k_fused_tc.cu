@@ -196,6 +196,10 @@ struct TcParams {
 #define HDC_I8_EPI_UNROLL 1
 #endif
 constexpr int kI8EpiUnroll = HDC_I8_EPI_UNROLL;
+#ifndef HDC_I8_EARLY
+#define HDC_I8_EARLY 1
+#endif
+constexpr bool kI8Early = HDC_I8_EARLY;            // int8 epilogue: release the accumulator after J
 #ifdef HDC_TC_DIAG_MASK
 // compile-time ablation (no runtime checks): DBG(m) is a constant
 #define DBG(mask) ((HDC_TC_DIAG_MASK) & (mask))
@@ -722,7 +726,45 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // is sub-tile cq (its three accumulators at 3 SUBN cq)
       const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE +
                              (CF::WIDE ? cq * 3 * SUBN : cq * EPI_COLS);
-      if constexpr (I8) {
+      bool released = false;                // accumulator buffer already handed back
+      if constexpr (I8 && kI8Early && CF::WIDE) {
+        // Two steps: (1) the accumulator -> J (four integer ops per element, J held in
+        // registers), then the buffer goes back to the Stage I issuer at once (the wide mode
+        // has one buffer, so this read is the part of the epilogue the MMAs wait for);
+        // (2) signs and flags from J (the test of the loop below, same J).  Wide mode only:
+        // with two buffers the read is hidden anyway, and the unrolled form cost cfg2 8%.
+        int32_t Jv[EPI_COLS];
+        constexpr int ECH = 8;              // columns per load group (registers: J + 3 x ECH)
+#pragma unroll
+        for (int ch = 0; ch < EPI_COLS / ECH; ++ch) {
+          const int cl = ch * ECH;
+          uint32_t r0[ECH], r1[ECH], r2[ECH];
+          tmem_ld8(tbase + cl, r0);
+          tmem_ld8(tbase + SUBN + cl, r1);
+          tmem_ld8(tbase + 2 * SUBN + cl, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < ECH; ++j)
+            Jv[cl + j] = ((int32_t)r0[j] << fsl) + ((int32_t)r1[j] >> fs1) + ((int32_t)r2[j] >> fs2);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_lead(tempty + buf);
+        released = true;
+#pragma unroll
+        for (int v = 0; v < EPI_COLS / 4; ++v) {
+          const int4 q4 = reinterpret_cast<const int4*>(scm)[v];
+          const int mq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int b = 4 * v + e;
+            const int32_t J = Jv[b];
+            const int32_t sg = J >> 31;
+            hbits[b >> 5] |= (uint32_t)sg & (1u << (b & 31));
+            if ((J ^ sg) - mq[e] <= mrow) flags[b >> 5] |= 1u << (b & 31);
+          }
+        }
+      } else if constexpr (I8) {
         // 64-bit masks (two for EPI_COLS = 80): register-resident under any unrolling
         static_assert(EPI_COLS <= 128, "int8 column group");
         uint64_t hb64 = 0, fl64 = 0, hb64x = 0, fl64x = 0;
@@ -793,10 +835,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
+      if (!released) {
+        tc_fence_before();
+        __syncwarp();
+      }
       if (lane == 0) {
-        arrive_lead(tempty + buf);                // accumulator free for tile t + 2
+        if (!released) arrive_lead(tempty + buf);   // accumulator free for tile t + NACC
         if (I8 && ENC) mbar_arrive(cempty + cs);   // encode mode: taus read
       }
       // H buffer hb free (Stage II of tile t - 2 done)
