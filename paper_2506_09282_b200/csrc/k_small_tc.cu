@@ -155,32 +155,87 @@ __global__ void __launch_bounds__(256) xlimb_image_kernel(const float* __restric
     reinterpret_cast<int64_t*>(img + (size_t)3 * NX * Fp)[n] = row_tau(l1, tau_const, valid && amax > 0.f);
 }
 
-// float64 re-evaluation of V[n, d] = x_n . b_d (exact fp32 products, fixed order: lane sums
-// f = lane, lane + 32, ... ascending, then a fixed butterfly) from copies of the two rows
-// staged in this warp's shared-memory scratch by bulk copies (one memory round trip for
-// F <= 1024 and little code: rarely executed code is fetched cold).  `xs` and `bs` hold
-// 1024 floats each (plus 4 of alignment slack for x).
+// float64 re-evaluation of V[n, d] = x_n . b_d (exact fp32 products, fixed order: lane
+// partial sums over f = lane + 128 i + 32 q for q = 0..3 (four independent chains: a single
+// chain of convert + FMA latencies cost ~1 us at F = 784), combined (q0 + q1) + (q2 + q3),
+// then a fixed butterfly) from copies of the two rows staged in this warp's shared-memory
+// scratch by bulk copies (one memory round trip for F <= 1024 and little code: rarely
+// executed code is fetched cold).  `xs` and `bs` hold 1024 floats each (plus 4 of alignment
+// slack for x).
+__device__ __forceinline__ void recheck_issue(const float* __restrict__ xr, const float* __restrict__ br, int F,
+                                              int f0, float* xs, float* bs, uint64_t* bar, int lane) {
+  const int len = F - f0 < 1024 ? F - f0 : 1024;
+  const uint64_t xa = reinterpret_cast<uint64_t>(xr + f0);
+  const int xo = (int)((xa & 15u) >> 2);
+  const uint32_t xb = (uint32_t)(((xo + len) * 4 + 15) & ~15), bb = (uint32_t)((len * 4 + 15) & ~15);
+  __syncwarp();
+  if (lane == 0) {
+    mbar_arrive_expect_tx(bar, xb + bb);
+    bulk_load(xs, reinterpret_cast<const void*>(xa & ~uint64_t(15)), xb, bar);
+    bulk_load(bs, br + f0, bb, bar);              // B^T rows are 256-byte aligned (Fp % 64 == 0)
+  }
+}
+// `issued`: the copies of the first 1024-element chunk were started earlier (recheck_issue).
 __device__ __noinline__ float recheck_smem(const float* __restrict__ xr, const float* __restrict__ br, int F,
-                                           float* xs, float* bs, uint64_t* bar, uint32_t& phase, int lane) {
-  double s = 0.0;
+                                           float* xs, float* bs, uint64_t* bar, uint32_t& phase, int lane,
+                                           bool issued = false) {
+  double s = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   for (int f0 = 0; f0 < F; f0 += 1024) {
     const int len = F - f0 < 1024 ? F - f0 : 1024;
-    const uint64_t xa = reinterpret_cast<uint64_t>(xr + f0);
-    const int xo = (int)((xa & 15u) >> 2);
-    const uint32_t xb = (uint32_t)(((xo + len) * 4 + 15) & ~15), bb = (uint32_t)((len * 4 + 15) & ~15);
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar, xb + bb);
-      bulk_load(xs, reinterpret_cast<const void*>(xa & ~uint64_t(15)), xb, bar);
-      bulk_load(bs, br + f0, bb, bar);            // B^T rows are 256-byte aligned (Fp % 64 == 0)
-    }
+    const int xo = (int)((reinterpret_cast<uint64_t>(xr + f0) & 15u) >> 2);
+    if (!(issued && f0 == 0)) recheck_issue(xr, br, F, f0, xs, bs, bar, lane);
     mbar_wait(bar, phase);
     phase ^= 1u;
+    int f = lane;
 #pragma unroll 1
-    for (int f = lane; f < len; f += 32) s = fma((double)xs[xo + f], (double)bs[f], s);
+    for (; f + 96 < len; f += 128) {
+      s = fma((double)xs[xo + f], (double)bs[f], s);
+      s1 = fma((double)xs[xo + f + 32], (double)bs[f + 32], s1);
+      s2 = fma((double)xs[xo + f + 64], (double)bs[f + 64], s2);
+      s3 = fma((double)xs[xo + f + 96], (double)bs[f + 96], s3);
+    }
+#pragma unroll 1
+    for (; f < len; f += 32) s = fma((double)xs[xo + f], (double)bs[f], s);
   }
+  s = (s + s1) + (s2 + s3);
   s = warp_sum_xor(s);
   return s >= 0.0 ? 1.f : -1.f;
+}
+
+// Stage II of one CTA (see the call site).  Thread item = (class k, row pair n0, n0 + 1):
+// per 4 columns one 16-byte load of C[k] and one (broadcast) of the sign masks serve both
+// rows -- the shared-memory wavefronts, not the adds, bound this loop (a thread per (n, k)
+// took ~2900 cycles at N = 32, K = 10).  Per (n, k): four partial sums over the columns
+// j = 4 i + q, combined (q0 + q1) + (q2 + q3): a fixed order.
+__device__ __noinline__ void stage2_pass(const float* Cs, const uint32_t* hmask, int RB, int nrows, int K, int ncol,
+                                         int wt, double scale, unsigned long long* acc) {
+  const int items = K * ((nrows + 1) >> 1);
+  for (int it = wt; it < items; it += kWorkers) {
+    const int k = it % K, n0 = 2 * (it / K), n1 = n0 + 1;
+    const float* cr = Cs + k * RB;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+    int j = 0;
+#pragma unroll 4
+    for (; j + 3 < ncol; j += 4) {
+      const uint4 h4 = *reinterpret_cast<const uint4*>(hmask + j);
+      const float4 c4 = *reinterpret_cast<const float4*>(cr + j);
+      a0 += ((h4.x >> n0) & 1u) ? -c4.x : c4.x;
+      a1 += ((h4.y >> n0) & 1u) ? -c4.y : c4.y;
+      a2 += ((h4.z >> n0) & 1u) ? -c4.z : c4.z;
+      a3 += ((h4.w >> n0) & 1u) ? -c4.w : c4.w;
+      b0 += ((h4.x >> n1) & 1u) ? -c4.x : c4.x;
+      b1 += ((h4.y >> n1) & 1u) ? -c4.y : c4.y;
+      b2 += ((h4.z >> n1) & 1u) ? -c4.z : c4.z;
+      b3 += ((h4.w >> n1) & 1u) ? -c4.w : c4.w;
+    }
+    for (; j < ncol; ++j) {
+      a0 += ((hmask[j] >> n0) & 1u) ? -cr[j] : cr[j];
+      b0 += ((hmask[j] >> n1) & 1u) ? -cr[j] : cr[j];
+    }
+    atomicAdd(acc + (int64_t)n0 * K + k, (unsigned long long)llrint((double)((a0 + a1) + (a2 + a3)) * scale));
+    if (n1 < nrows)
+      atomicAdd(acc + (int64_t)n1 * K + k, (unsigned long long)llrint((double)((b0 + b1) + (b2 + b3)) * scale));
+  }
 }
 
 __device__ __forceinline__ void wbar() {          // the worker warps only (named barrier 1)
@@ -336,81 +391,92 @@ small_tc_kernel(const __grid_constant__ CUtensorMap tmB, const SmallTcParams p) 
     wbar();
     // float64 re-evaluation of the flagged signs, spread evenly over the 8 worker warps: every
     // warp scans the per-column flag counts (lane l: columns 4l .. 4l + 3) and takes flags
-    // e = ww, ww + 8, ... in column-major order; one warp per sign (fixed lane order); a
-    // flipped sign updates its column's mask bit (atomically: warps share columns)
+    // e = ww, ww + 8, ... in column-major order; one warp per sign (fixed lane order).  The
+    // row copies of a warp's first flag go out before Stage II, which runs on the
+    // provisional signs; a sign the re-evaluation flips then adds the exact correction
+    // (h - h') C[k, d] = 2 h C[k, d] to the int64 sums (Stage II is linear in H),
+    // so the recheck's round trip overlaps Stage II instead of preceding it.
+    const int wt = tid - 64;
+    const int nk = p.nrows * K;
     unsigned long long nrecheck = 0;
     uint32_t rphase = 0u;
-    {
-      uint32_t fw[4];
-      int cnt = 0;
+    uint32_t fw[4];
+    int cnt = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int jj = 4 * lane + u;
-        fw[u] = jj < ncol ? fmask[jj] : 0u;
-        cnt += __popc(fw[u]);
-      }
-      int incl = cnt;                              // inclusive prefix over lanes
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      for (int e = ww; e < total; e += kWarpsT - 2) {
-        const int L = __ffs(__ballot_sync(0xffffffffu, incl > e)) - 1;   // lane holding flag e
-        int jsel = 0, nsel = 0;
-        if (lane == L) {
-          int r = e - (incl - cnt);                  // rank of the flag within this lane's columns
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = __popc(fw[u]);
-            if (r >= 0 && r < c) {
-              uint32_t m = fw[u];
-              for (int t = 0; t < r; ++t) m &= m - 1;
-              jsel = 4 * lane + u;
-              nsel = __ffs(m) - 1;
-            }
-            r -= c;
-          }
-        }
-        jsel = __shfl_sync(0xffffffffu, jsel, L);
-        nsel = __shfl_sync(0xffffffffu, nsel, L);
-        // the ring is free once the MMAs are done (tfull): 8 KB of it per warp as scratch
-        float* xs = reinterpret_cast<float*>(ring + (size_t)ww * 8208);
-        const float hv = recheck_smem(p.X + (int64_t)nsel * p.F, p.Bt + (d0 + jsel) * p.Fp, (int)p.F, xs,
-                                      xs + 1028, rbar + ww, rphase, lane);
-        if (lane == 0) {
-          if (hv < 0.f) atomicOr(hmask + jsel, 1u << nsel);
-          else atomicAnd(hmask + jsel, ~(1u << nsel));
-        }
-        ++nrecheck;
-      }
+    for (int u = 0; u < 4; ++u) {
+      const int jj = 4 * lane + u;
+      fw[u] = jj < ncol ? fmask[jj] : 0u;
+      cnt += __popc(fw[u]);
     }
-    wbar();                                          // hmask final before Stage II
+    int incl = cnt;                                // inclusive prefix over lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    auto select = [&](int e, int& jsel, int& nsel) {   // column and row of flag e
+      const int L = __ffs(__ballot_sync(0xffffffffu, incl > e)) - 1;   // lane holding flag e
+      jsel = 0;
+      nsel = 0;
+      if (lane == L) {
+        int r = e - (incl - cnt);                  // rank of the flag within this lane's columns
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = __popc(fw[u]);
+          if (r >= 0 && r < c) {
+            uint32_t m = fw[u];
+            for (int t = 0; t < r; ++t) m &= m - 1;
+            jsel = 4 * lane + u;
+            nsel = __ffs(m) - 1;
+          }
+          r -= c;
+        }
+      }
+      jsel = __shfl_sync(0xffffffffu, jsel, L);
+      nsel = __shfl_sync(0xffffffffu, nsel, L);
+    };
+    // the ring is free once the MMAs are done (tfull): 8 KB of it per warp as scratch
+    float* xs = reinterpret_cast<float*>(ring + (size_t)ww * 8208);
+    int j0 = 0, n0 = 0;
+    if (ww < total) {
+      select(ww, j0, n0);
+      recheck_issue(p.X + (int64_t)n0 * p.F, p.Bt + (d0 + j0) * p.Fp, (int)p.F, 0, xs, xs + 1028, rbar + ww, lane);
+    }
+    if (ww == 0) T_REC(11);
+    // ---- Stage II: S_local[n][k] = sum_{d in range} h[n, d] C[k, d] on the
+    // provisional signs; exact int64 fixed-point accumulation across CTAs (Alg. 3
+    // `S += S_local`).  Four independent partial sums over columns j = 4 i + q
+    // (16-byte loads of C and the sign masks; RB is a multiple of 4), combined
+    // (q0 + q1) + (q2 + q3): fixed order.
+    stage2_pass(Cs, hmask, RB, p.nrows, K, ncol, wt, p.scale, p.acc);
+    if (ww == 0) T_REC(12);
+    for (int e = ww; e < total; e += kWarpsT - 2) {
+      int jsel = j0, nsel = n0;
+      if (e != ww) select(e, jsel, nsel);
+      const float hv = recheck_smem(p.X + (int64_t)nsel * p.F, p.Bt + (d0 + jsel) * p.Fp, (int)p.F, xs,
+                                    xs + 1028, rbar + ww, rphase, lane, e == ww);
+      const bool prov_neg = (hmask[jsel] >> nsel) & 1u;
+      if ((hv < 0.f) != prov_neg) {                 // flipped: S[n, k] += (h - h') C[k, d]
+        const float dh = hv < 0.f ? -2.f : 2.f;
+        for (int k = lane; k < K; k += 32) {
+          const long long v = llrint((double)(dh * Cs[k * RB + jsel]) * p.scale);
+          atomicAdd(p.acc + (int64_t)nsel * K + k, (unsigned long long)v);
+        }
+      }
+      ++nrecheck;
+    }
     if (lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
   }
-  __syncthreads();                                   // TMEM reads and rechecks done (all warps)
+  __syncthreads();                                   // TMEM reads, Stage II and rechecks done (all warps)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<128>(tmem);
   }
   if (warp < 2) return;
-
-  // ---- Stage II: S_local[n][k] = sum_{d in range} h[n, d] C[k, d], d ascending;
-  // then exact int64 fixed-point accumulation across CTAs (Alg. 3 `S += S_local`)
+  if (tid == 64) T_REC(13);
   const int wt = tid - 64;
   const int nk = p.nrows * K;
-  for (int i = wt; i < nk; i += kWorkers) {
-    const int n = i / K, k = i - n * K;
-    const float* cr = Cs + k * RB;
-    float s = 0.f;
-    for (int j = 0; j < ncol; ++j) {
-      const float cv = cr[j];
-      s += ((hmask[j] >> n) & 1u) ? -cv : cv;
-    }
-    const long long v = llrint((double)s * p.scale);
-    atomicAdd(p.acc + i, (unsigned long long)v);
-  }
   T_MARK(4);
   if (wt == 0) T_REC(9);
   wbar();
@@ -496,7 +562,7 @@ cudaError_t launch_nx(const CUtensorMap& tm, SmallTcParams& p, uint8_t* img, cud
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "[hdc small_tc cta0]");
-    for (int i = 0; i < 11; ++i) fprintf(stderr, " %d:%.2f", i, h[8 + i] ? ((double)(long long)(h[8 + i] - h[0])) * 1e-3 : -1.0);
+    for (int i = 0; i < 14; ++i) fprintf(stderr, " %d:%.2f", i, h[8 + i] ? ((double)(long long)(h[8 + i] - h[0])) * 1e-3 : -1.0);
     fprintf(stderr, "\n[hdc small_tc debug] NX=%d G=%d RB=%d nst=%d: from first CTA start (us): X limbs %.2f, "
             "MMA done %.2f, signs %.2f, stage II %.2f, final %.2f\n", NX, p.G, p.RB, p.nst, (h[1] - h[0]) * 1e-3,
             (h[2] - h[0]) * 1e-3, (h[3] - h[0]) * 1e-3, (h[4] - h[0]) * 1e-3, h[5] ? (h[5] - h[0]) * 1e-3 : -1.0);
