@@ -6,10 +6,11 @@
 //             (eq. batch_encode);
 //   act       HardSign in the epilogue warps after tcgen05.ld, written
 //             as exact bf16 +-1 into TMEM (bf16/tf32) or a shared-memory H tile (int8);
-//   Stage II  S[n, :] += H_tile C_tile^T as a second tcgen05.mma (bf16, C split
-//             into hi + lo bf16 parts) into a TMEM accumulator that lives for the
-//             CTA's whole run of D-tiles of one N-tile (eq. batch_sim P:180-183;
-//             ScalableHD-L row ownership, Alg. 4).
+//   Stage II  S_t = H_tile C_tile^T as a second tcgen05.mma (bf16; C split into
+//             hi + lo bf16 parts, hi + mid + lo = C exactly in the int8 modes) into a
+//             TMEM accumulator, drained per tile into exact int64 fixed-point row sums
+//             that live for the CTA's whole run of D-tiles of one N-tile (eq. batch_sim
+//             P:180-183; ScalableHD-L row ownership, Alg. 4).
 // H never leaves the SM.
 //
 // Precision modes (hdc_precision_t):
@@ -18,8 +19,10 @@
 //   INT8x3 (HDC_PREC_FP32_TC, sign-exact): per-row/column scaled 21-bit integer
 //         images of X and B split into three balanced base-128 int8 limbs; the
 //         six limb products with i + j <= 2 run as three N-concatenated kind::i8
-//         MMAs with EXACT int32 accumulation into three TMEM accumulators (BN = 80),
-//         combined in int64.  The rigorous bound of that integer image (DESIGN.md
+//         MMAs with EXACT int32 accumulation into three TMEM accumulators (BN = 80,
+//         double-buffered; or the "wide" mode for large F: BN = 160 as two 80-column
+//         sub-tiles, one buffer), combined in int64.  The rigorous bound of that integer
+//         image (DESIGN.md
 //         §4) flags the few |I| <= tau; they are re-evaluated in float64 after the
 //         kernel (tc_recheck_kernel), so every HardSign decision equals that of
 //         the exact product X B and S is corrected exactly where a sign flips.
@@ -29,12 +32,10 @@
 // owner), warp 2 C-tile producer, warp 3 Stage II MMA issuer, warps 4..11 epilogue.
 // Operand ring: SWIZZLE_128B K-major stages (64-byte SWIZZLE_64B int8 stages when
 // Fp % 128 != 0).  Clusters: 2x1 CTAs sharing each B tile by TMA multicast (default),
-// single CTAs for one N-tile, virtual 1 x 4 / 1 x 8 groups when the live X tiles plus
-// B exceed L2, or a cta_group::2 pair (HDC_TC_CLUSTER=2x1p).  Time per tile = the MMA
-// floor of its K stages + ~2000 cycles the pipeline does not hide (epilogue TMEM traffic,
-// Stage II, operand TMA).  Partial scores of N-tiles split between clusters are
-// summed in a fixed order by the last arriver, which takes the lowest-index argmax:
-// bit-deterministic.
+// single CTAs for one N-tile, virtual 1 x 4 / 1 x 8 / 1 x 16 groups when the live X tiles
+// plus B exceed L2, or a cta_group::2 pair (HDC_TC_CLUSTER=2x1p).  Partial scores of
+// N-tiles split between clusters are exact int64 sums, added by the last arriver, which
+// takes the lowest-index argmax: bit-deterministic and independent of N.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -81,7 +82,7 @@ constexpr int KP_MAX_16 = 64;
 
 // D-tile width by mode and class count: 160 for bf16/tf32 with K <= 32 (an N=160
 // MMA costs the same cycles as N=80, tools/mma_microbench.cu), else 80
-// (int8: three limb accumulators x 80 columns x 2 buffers fill TMEM).
+// (int8: three limb accumulators x 80 columns x 2 buffers fill TMEM; wide: 2 x 3 x 80, one buffer).
 // mode 3 = the int8 mode with 160-column tiles made of two 80-column sub-tiles and ONE
 // accumulator buffer ("wide", large F only): each A (X limb) stage feeds twice the MMA work,
 // so the operand stream per MMA cycle falls from 81 to 56 bytes per SM
@@ -112,9 +113,9 @@ struct Cfg {
   static constexpr int KA = KBYTES / ESZ;                        // K elements per atom
   static constexpr int KE = NAT * KA;                            // K elements per stage
   static constexpr int KP_MAX = WIDE ? 16 : (I8 || BN > 80) ? KP_MAX_I8 : KP_MAX_16;
-  // TMEM columns: two Stage I accumulator buffers, the Stage II accumulator (hi and lo C
-  // parts accumulate into the same Kp columns) and, for bf16/tf32, two H tiles as the
-  // Stage II A operand (bf16 pairs, BN/2 columns each).
+  // TMEM columns: NACC Stage I accumulator buffers, the Stage II accumulator (the C parts
+  // accumulate into the same Kp columns) and, for bf16/tf32, two H tiles as the Stage II
+  // A operand (bf16 pairs, BN/2 columns each).
   static constexpr int ACC_STRIDE = I8 ? 3 * BN : (BN <= 128 ? 128 : BN);
   static constexpr int D2_COL = NACC * ACC_STRIDE;
   static constexpr bool H_TMEM = !I8;
