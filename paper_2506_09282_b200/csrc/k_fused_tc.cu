@@ -705,18 +705,21 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         while (!mbar_test(tfull + buf, bphase)) __nanosleep(500);
       }
       TWAIT(6, tfull + buf, bphase);
+      // wide mode (one accumulator buffer): the S drain and the wait for the column taus come
+      // after the accumulator is handed back, off the Stage I issuer's critical path
+      constexpr bool kLate = I8 && kI8Early && CF::WIDE;
       // Stage II of two tiles back: issued a whole tile ago, so complete; draining it lets the
       // Stage II MMAs of the previous tile go out (one TMEM accumulator, drained in order)
-      if (!ENC)
+      if (!ENC && !kLate)
         while (next_drain <= t - 2) {
           drain_s();
           ++next_drain;
         }
       const int32_t* scm = nullptr;         // coarse column taus of this tile (int8 mode), in smem
-      if constexpr (I8) {
+      static_assert((EPI_COLS * 4) % 16 == 0, "16-byte column-tau loads");
+      if constexpr (I8 && !kLate) {
         TWAIT(15, cfull + cs, cphase);
         scm = reinterpret_cast<const int32_t*>(sC + cs * CF::C_SLOT + c_tile_bytes) + cq * EPI_COLS;
-        static_assert((EPI_COLS * 4) % 16 == 0, "16-byte column-tau loads");
       }
       tc_fence_after();
       // ---- phase 1: accumulator -> HardSign bits (bit set -> h = -1) and recheck flags
@@ -752,6 +755,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         __syncwarp();
         if (lane == 0) arrive_lead(tempty + buf);
         released = true;
+        if (!ENC)
+          while (next_drain <= t - 2) {
+            drain_s();
+            ++next_drain;
+          }
+        TWAIT(15, cfull + cs, cphase);
+        scm = reinterpret_cast<const int32_t*>(sC + cs * CF::C_SLOT + c_tile_bytes) + cq * EPI_COLS;
 #pragma unroll
         for (int v = 0; v < EPI_COLS / 4; ++v) {
           const int4 q4 = reinterpret_cast<const int4*>(scm)[v];
