@@ -159,6 +159,7 @@ struct TcParams {
   int64_t N, F, Fp, D, Dp, Dq, K, Kp, Np;
   int Tn, Td, G;            // G = clusters of the launch
   int TdG;                  // D-groups: a cluster tile = CLN N-tiles x CLD consecutive D-tiles
+  int runit;                // range granularity in cluster tiles: TdG = whole N-tile rows per cluster
   int64_t T;                // cluster tiles (n-major), contiguous ranges per cluster
   const float* X;          // caller's X (fp64 recheck)
   const float* Bt;         // fp32 B^T [Dp][Fp] (fp64 recheck)
@@ -249,11 +250,15 @@ __device__ __noinline__ void watchdog_wait(const P& p, uint64_t* bar, uint32_t p
     }                                                                \
   } while (0)
 
-__device__ __forceinline__ int64_t range_begin(int c, int64_t T, int G) { return (int64_t)c * T / G; }
-__device__ __forceinline__ int owner_of(int64_t t, int64_t T, int G) {
+// Contiguous ranges of the n-major cluster-tile sequence, in units of U tiles (U = TdG: every
+// range is whole N-tile rows, so the groups sweep the D-groups of B in step)
+__device__ __forceinline__ int64_t range_begin(int c, int64_t T, int G, int U) {
+  return (int64_t)c * (T / U) / G * U;
+}
+__device__ __forceinline__ int owner_of(int64_t t, int64_t T, int G, int U) {
   int c = (int)((t * G) / T);
-  while (c + 1 < G && range_begin(c + 1, T, G) <= t) ++c;
-  while (c > 0 && range_begin(c, T, G) > t) --c;
+  while (c + 1 < G && range_begin(c + 1, T, G, U) <= t) ++c;
+  while (c > 0 && range_begin(c, T, G, U) > t) --c;
   return c;
 }
 
@@ -340,7 +345,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint16_t b_mask = 0;                                                    // same D-tile
 #pragma unroll
   for (int i = 0; i < CLN; ++i) b_mask |= (uint16_t)(1u << (i * CLD + rd));
-  const int64_t t0 = range_begin(cl, p.T, p.G), t1 = range_begin(cl + 1, p.T, p.G);
+  const int64_t t0 = range_begin(cl, p.T, p.G, p.runit), t1 = range_begin(cl + 1, p.T, p.G, p.runit);
   // K stages; the int8 mode's 128-byte stages may overhang Fp (a multiple of 64) by 64
   // elements: TMA zero-fills past the tensor's extent and the MMA skips those k-steps
   const int KB = (int)((p.Fp + KE - 1) / KE);
@@ -987,8 +992,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // the row's classes of column group cq.  The N-tile's D-groups are split over clusters
       // c_first..c_last, each over its CLD ranks; the partial sums are integers, so their
       // total (and every score) is independent of the split.
-      const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G);
-      const int c_last = owner_of((int64_t)(ng + 1) * p.TdG - 1, p.T, p.G);
+      const int c_first = owner_of((int64_t)ng * p.TdG, p.T, p.G, p.runit);
+      const int c_last = owner_of((int64_t)(ng + 1) * p.TdG - 1, p.T, p.G, p.runit);
       const bool sole = (c_first == c_last) && CLD == 1;
       const int kq0 = cq * kq;                // first class of this thread's group
       if (sole) {
@@ -1030,7 +1035,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int P = (c_last - c_first + 1) * CLD;     // partials per row of this N-tile
       // slot of this N-tile in a contributing CTA's S_part: clusters after c_first start
       // inside N-group ng (slot 0); c_first may have started in an earlier one
-      const int ng_first = (int)(range_begin(c_first, p.T, p.G) / p.TdG);
+      const int ng_first = (int)(range_begin(c_first, p.T, p.G, p.runit) / p.TdG);
       const int slot_first = (CLD == 1) ? ((ng_first == ng) ? 0 : 1) : (ng - ng_first);
       auto part_ptr = [&](int idx, int r, int k) {   // partial idx (cluster-major, then D rank)
         const int cc = c_first + idx / CLD, j = idx % CLD;
@@ -1450,7 +1455,16 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     if (dev >= 0 && dev < kMaxDev) cache[dev].store(n);
   }
   p.G = (int)(p.T < max_clusters ? p.T : max_clusters);
-  const int64_t per = (p.T + p.G - 1) / p.G;    // cluster tiles per range (at most)
+  // whole N-tile rows per range when there are many per cluster (imbalance <= 1/8 row): the
+  // groups then sweep B's D-groups in step, so a B chunk fetched from DRAM serves all of them
+  // from L2 (cfg5 int8 17.5 -> 17.1-17.3 ms, D = 20000 36.5 -> 34.1, bf16 6.95 -> 6.80);
+  // HDC_TC_ALIGN=0 restores tile-granular ranges (measurements)
+  {
+    const char* al = getenv("HDC_TC_ALIGN");
+    const bool align = al ? atoi(al) != 0 : true;
+    p.runit = (align && p.TdG > 1 && p.T / p.TdG >= 8 * (int64_t)p.G) ? p.TdG : 1;
+  }
+  const int64_t per = (p.T / p.runit + p.G - 1) / p.G * p.runit;   // cluster tiles per range (at most)
   p.nslot = (CLD == 1) ? 2 : (int)((per + p.TdG - 1) / p.TdG + 1);
   if ((int64_t)p.G * CLS * p.nslot > p.s_part_cap) return cudaErrorInvalidValue;   // workspace bound
   cfg.gridDim = dim3(p.G * CLS, 1, 1);
