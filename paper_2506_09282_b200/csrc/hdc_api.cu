@@ -261,8 +261,12 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   const int mode = tc_mode_of(m);
   const int64_t gm = kTileM * m->cl_n;
   const int64_t Np = (N + gm - 1) / gm * gm;
-  const int64_t slots = tc_s_part_slots(Np / kTileM, m->Dq / tc_tile_n(mode, m->K), m->cl_n, m->cl_d,
-                                        m->cl_virt, m->num_sms);
+  int64_t slots = tc_s_part_slots(Np / kTileM, m->Dq / tc_tile_n(mode, m->K), m->cl_n, m->cl_d,
+                                  m->cl_virt, m->num_sms);
+  if (m->cl_virt == 1 && m->cl_d > 4) {            // run_fused_tc may launch 1 x 4 groups
+    const int64_t s4 = tc_s_part_slots(Np / kTileM, m->Dq / tc_tile_n(mode, m->K), 1, 4, 1, m->num_sms);
+    if (s4 > slots) slots = s4;
+  }
   if (Np <= m->tw_rows && slots <= m->tw_slots) return HDC_OK;
   const int64_t rows = Np > m->tw_rows ? Np : m->tw_rows;
   const int64_t nsl = slots > m->tw_slots ? slots : m->tw_slots;
@@ -325,6 +329,13 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
     cl_d = 1;
     cl_virt = 0;
   }
+  // large batches on virtual groups: 1 x 4 groups once every group gets >= 8 rows of N-tiles,
+  // so the launch takes ranges of whole rows and the groups sweep B's D-groups in step
+  // (k_fused_tc.cu launch_mode): cfg5 int8 17.1 -> 16.7-16.8 ms, bf16 6.69 -> 6.07, D = 2000
+  // bf16 2.81 -> 1.64; below that 1 x 16 (N = 16384: int8 2.08 vs 2.34 ms)
+  if (cl_virt == 1 && cl_d > 4 && !getenv("HDC_TC_CLUSTER") &&
+      (N + kTileM - 1) / kTileM >= 8 * (int64_t)(m->num_sms / 4))
+    cl_d = 4;
   const int64_t gm = kTileM * cl_n;
   const int64_t Np = (N + gm - 1) / gm * gm;
   cudaError_t e;
