@@ -481,15 +481,11 @@ small_tc_kernel(const __grid_constant__ CUtensorMap tmB, const SmallTcParams p) 
   if (wt == 0) T_REC(9);
   wbar();
   if (wt == 0) {
-    // release: this CTA's reductions are ordered before its arrival is counted
+    // acq_rel: this CTA's reductions are ordered before its arrival is counted (release), and
+    // the last arriver sees every other CTA's (acquire) -- one round trip
     unsigned prev;
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt) : "memory");
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt) : "memory");
     *s_last = (prev == (unsigned)(p.G - 1)) ? 1 : 0;
-    if (*s_last) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p.cnt) : "memory");   // every CTA's release
-      (void)v;
-    }
   }
   wbar();
   if (!*s_last) return;

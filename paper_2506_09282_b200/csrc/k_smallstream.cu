@@ -319,15 +319,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   cbar();
   SS_MARK(3);
   if (tid == 0) {
-    unsigned prev;   // release: this CTA's additions are ordered before its arrival is counted
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt) : "memory");
+    // acq_rel: this CTA's additions are ordered before its arrival is counted (release), and
+    // the last arriver sees every other CTA's (acquire) -- one round trip
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt) : "memory");
     s_last = (prev == (unsigned)(p.G - 1)) ? 1 : 0;
-    if (s_last) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p.cnt) : "memory");
-      (void)v;
-      p.cnt[0] = 0u;
-    }
+    if (s_last) p.cnt[0] = 0u;
   }
   cbar();
   if (!s_last) return;
