@@ -231,7 +231,7 @@ int32_t hdc_model_last_kernel(hdc_model_t m);
 
 /* D-tile width of this model's fused tensor-core kernel (diagnostic): 80 or 160 columns,
  * 0 if the model has no tensor-core path, -1 on a NULL model.  int8 models (fp32_tc, and
- * fp32 when routed) with K <= 16 and padded F >= 2048 run the "wide" K4 variant, 160-column
+ * fp32 when routed) with K <= 16 and padded F >= 768 run the "wide" K4 variant, 160-column
  * tiles of two 80-column sub-tiles; the environment variable HDC_TC_WIDE=0/1,
  * read at model creation, overrides the F threshold (measurements). */
 int32_t hdc_model_tc_tile_n(hdc_model_t m);

@@ -54,7 +54,8 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 constexpr int64_t kMaxF = int64_t(1) << 20;
 constexpr int kSmallMaxN = 32;
 constexpr int kSmallMaxNLowp = 8;          // bf16 / tf32 models (see run())
-constexpr int64_t kWideMinFp = 2048;       // int8 wide K4 from this padded F (cfg5: 3072)
+constexpr int64_t kWideMinFp = 768;        // int8 wide K4 from this padded F (tools/gpu/r2_wsweep.py:
+                                           // wide/80-column time 1.0-1.02 at F = 640, 0.93-0.95 at 784)
 constexpr int kSmallTcMinN = 5;            // fp32_tc models: K2t from this many rows (see run())
 constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 

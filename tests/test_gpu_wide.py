@@ -1,6 +1,6 @@
 """GPU parity of K4's int8 "wide" mode (160-column tiles of two 80-column sub-tiles, one
 accumulator buffer), the default for fp32-semantics models with K <= 16 and
-padded F >= 2048, forced elsewhere with HDC_TC_WIDE=1 (read at model creation).
+padded F >= 768, forced elsewhere with HDC_TC_WIDE=1 (read at model creation).
 
 The wide mode changes the tile width of the sign-exact Stage I and the Stage II tile sums,
 not the arithmetic contract: results must meet the fp32 policy against the oracle."""
@@ -43,7 +43,7 @@ def test_wide_forced_edge_grid(hdc, monkeypatch, N, F, D, K):
 
 
 def test_wide_default_by_F(hdc, monkeypatch):
-    """Padded F >= 2048 and K <= 16 select the wide mode; K > 16 or smaller F do not."""
+    """Padded F >= 768 and K <= 16 select the wide mode; K > 16 or smaller F do not."""
     monkeypatch.delenv("HDC_TC_WIDE", raising=False)
     X, B, C = _inputs(150, 2100, 500, 10, 5)
     Bd, Cd = to_dev(B, C)
