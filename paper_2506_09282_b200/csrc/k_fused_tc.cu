@@ -436,10 +436,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
               const int xk = kb * KE + a * CF::KA;
               if constexpr (MC && CLD > 1) tma_load_2d_mc(da, &tmA, full + stage, xk, ya, a_mask);
               else tma_load_2d(da, &tmA, full + stage, xk, ya);
-              // B stage layout [sub-tile][limb][SUBN rows]: each sub-tile's [b0; b1; b2] contiguous
+              // B stage layout: [b0; b1; b2] (80-column mode), or the wide mode's row blocks
+              // [b0s0 b0s1 b2s0 b2s1 b1s0 b1s1] (tc_mma_i8w5_elect)
 #pragma unroll
               for (int h = 0; h < NSUB; ++h) {
-                uint8_t* db = sB + stage * CF::B_STAGE + (h * NL + l) * (CF::B_LIMB_BYTES / NSUB) +
+                const int blk = CF::WIDE ? (l == 0 ? 0 : l == 2 ? 2 : 4) + h : l;
+                uint8_t* db = sB + stage * CF::B_STAGE + blk * (CF::B_LIMB_BYTES / NSUB) +
                               a * CF::ATOM_B + rb * BR * KBYTES;
                 const int yb = (int)(l * p.Dq + (int64_t)di * BN + h * SUBN + rb * BR);
                 if constexpr (MC && CLN > 1) tma_load_2d_mc(db, &tmB, full + stage, xk, yb, b_mask);
@@ -485,16 +487,22 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             //   [A0|A1|A2] (+)= x0 [b0;b1;b2]^T,  [A1|A2] += x1 [b0;b1]^T,  A2 += x2 b0^T
             // (each A tile is read from shared memory once per k-step, not 3 times).
             // Wide mode: the same for each 80-column sub-tile h, accumulators at 240 h.
+            // Wide mode: the five MMAs of tc_mma_i8w5_elect over both sub-tiles.
             const int nks = (kb == KB - 1) ? last_ks : KBYTES / 32;
 #pragma unroll
             for (int ks = 0; ks < KBYTES / 32; ++ks)
-              if (ks < nks)
-#pragma unroll
-                for (int h = 0; h < NSUB; ++h)
-                  tc_mma_i8x3_elect(acc0 + h * 3 * SUBN, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
-                                    a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4),
-                                    b_d + ((h * 3 * SUBN * KBYTES) >> 4) + 2 * ks, IDESC_N240, IDESC_N160,
-                                    IDESC, SUBN, ks == 0 ? acc : 1u);
+              if (ks < nks) {
+                if constexpr (CF::WIDE)
+                  tc_mma_i8w5_elect(acc0, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
+                                    a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks,
+                                    b_d + ((3 * SUBN * KBYTES) >> 4) + 2 * ks,
+                                    b_d + ((4 * SUBN * KBYTES) >> 4) + 2 * ks, IDESC_N240, IDESC_N160,
+                                    ks == 0 ? acc : 1u);
+                else
+                  tc_mma_i8x3_elect(acc0, a_d + 2 * ks, a_d + ((A_LIMB_BYTES + ks * 32) >> 4),
+                                    a_d + ((2 * A_LIMB_BYTES + ks * 32) >> 4), b_d + 2 * ks, IDESC_N240,
+                                    IDESC_N160, IDESC, SUBN, ks == 0 ? acc : 1u);
+              }
           } else {
             const int nat = (kb == KB - 1) ? last_at : CF::NAT;
 #pragma unroll
@@ -731,10 +739,11 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       uint32_t hbits[NWB], flags[NWB];
 #pragma unroll
       for (int w = 0; w < NWB; ++w) hbits[w] = flags[w] = 0u;
-      // int8: limb accumulators A0 | A1 | A2 of SUBN columns each; wide mode: column group cq
-      // is sub-tile cq (its three accumulators at 3 SUBN cq)
-      const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE +
-                             (CF::WIDE ? cq * 3 * SUBN : cq * EPI_COLS);
+      // int8: limb accumulators A0 | A1 | A2 of SUBN columns each at tbase + {0, 1, 2} SUBN;
+      // wide mode: column group cq is sub-tile cq, its accumulators in the blocks
+      // [A0s0 A0s1 A2s0 A2s1 A1s0 A1s1] (tc_mma_i8w5_elect): A0 at cq, A1 at 4 + cq, A2 at 2 + cq
+      const uint32_t tbase = tmem_base + lane_off + buf * CF::ACC_STRIDE + (CF::WIDE ? cq * SUBN : cq * EPI_COLS);
+      constexpr uint32_t OFF_A1 = CF::WIDE ? 4 * SUBN : SUBN, OFF_A2 = CF::WIDE ? 2 * SUBN : 2 * SUBN;
       bool released = false;                // accumulator buffer already handed back
       if constexpr (I8 && kI8Early && CF::WIDE) {
         // Two steps: (1) the accumulator -> J (four integer ops per element, J held in
@@ -749,8 +758,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const int cl = ch * ECH;
           uint32_t r0[ECH], r1[ECH], r2[ECH];
           tmem_ld8(tbase + cl, r0);
-          tmem_ld8(tbase + SUBN + cl, r1);
-          tmem_ld8(tbase + 2 * SUBN + cl, r2);
+          tmem_ld8(tbase + OFF_A1 + cl, r1);
+          tmem_ld8(tbase + OFF_A2 + cl, r2);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < ECH; ++j)
@@ -790,12 +799,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           uint32_t r0[CH], r1[CH], r2[CH];
           if constexpr (CH == 16) {
             tmem_ld16(tbase + cl, r0);
-            tmem_ld16(tbase + SUBN + cl, r1);
-            tmem_ld16(tbase + 2 * SUBN + cl, r2);
+            tmem_ld16(tbase + OFF_A1 + cl, r1);
+            tmem_ld16(tbase + OFF_A2 + cl, r2);
           } else {
             tmem_ld8(tbase + cl, r0);
-            tmem_ld8(tbase + SUBN + cl, r1);
-            tmem_ld8(tbase + 2 * SUBN + cl, r2);
+            tmem_ld8(tbase + OFF_A1 + cl, r1);
+            tmem_ld8(tbase + OFF_A2 + cl, r2);
           }
           tmem_ld_wait();
           uint32_t hc = 0, fc = 0;            // this chunk's bits

@@ -328,6 +328,29 @@ __device__ __forceinline__ void tc_mma_i8x3_elect(uint32_t d0, uint64_t a0, uint
       : "memory");
 }
 
+// One int8 k-step of the wide mode (two 80-column sub-tiles s0, s1; see k_fused_tc.cu):
+// TMEM accumulator blocks [A0s0 A0s1 A2s0 A2s1 A1s0 A1s1] and B row blocks
+// [b0s0 b0s1 b2s0 b2s1 b1s0 b1s1], 80 columns / rows each, so the six limb products of both
+// sub-tiles are five MMAs of N = 240, 240, 160, 160, 160 (an N <= 160 MMA costs as much as
+// N = 160: tools/mma_microbench.cu):
+//   x0 [b0s0 b0s1 b2s0] -> [A0s0 A0s1 A2s0]      x0 [b2s1 b1s0 b1s1] -> [A2s1 A1s0 A1s1]
+//   x1 [b0s0 b0s1] -> [A1s0 A1s1]      x1 [b1s0 b1s1] -> [A2s0 A2s1]      x2 [b0s0 b0s1] -> [A2s0 A2s1]
+// b0 / b3 / b4: descriptors of row blocks 0 / 3 / 4.
+__device__ __forceinline__ void tc_mma_i8w5_elect(uint32_t d0, uint64_t a0, uint64_t a1, uint64_t a2,
+                                                  uint64_t b0, uint64_t b3, uint64_t b4, uint32_t i240,
+                                                  uint32_t i160, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 d1, d2, d3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %9, 0;\n\tadd.u32 d1, %0, 240;\n\tadd.u32 d2, %0, 320;\n\tadd.u32 d3, %0, 160;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %4, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], %1, %5, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], %2, %4, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], %2, %6, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [d3], %3, %4, %8, 1;\n\t}" ::"r"(d0),
+      "l"(a0), "l"(a1), "l"(a2), "l"(b0), "l"(b3), "l"(b4), "r"(i240), "r"(i160), "r"(accumulate)
+      : "memory");
+}
+
 // CTA-pair (cta_group::2, M = 256) forms, issued by the leader CTA only: A rows 0-127
 // from the leader's shared memory / TMEM lanes, 128-255 from the peer's; B's N extent
 // split, the first half from the leader, the second from the peer (same offsets).

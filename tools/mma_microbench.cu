@@ -74,7 +74,9 @@ int main() {
   run<0, 160, 2, 1024, false, true>("bf16 N=160 distinct tiles", blocks);
   run<0, 256, 2, 1024, false, true>("bf16 N=256 distinct tiles", blocks);
   run<2, 80, 4, 512, false, true>("i8 N=80 SW64 distinct", blocks);
+  run<2, 160, 4, 512, false, true>("i8 N=160 SW64 distinct", blocks);
   run<2, 240, 4, 512, false, true>("i8 N=240 SW64 distinct", blocks);
+  run<2, 256, 4, 512, false, true>("i8 N=256 SW64 distinct", blocks);
   run<2, 240, 2, 1024, false, true>("i8 N=240 SW128 distinct", blocks);
   run<0, 32, 0, 0, true, false>("bf16 N=32 interleaved", blocks);
   return 0;
