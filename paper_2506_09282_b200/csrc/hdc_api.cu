@@ -71,6 +71,8 @@ struct hdc_model_s {
   float* Bp = nullptr;
   float* Bt = nullptr;
   float* B4 = nullptr;       // unit-major copy of Bp for the small-batch kernel
+  uint16_t* B4h = nullptr;   // its bf16 hi plane (K2s sign-exact streaming: half the bytes)
+  float* hibound = nullptr;  // [Dp] the hi plane's sign-bound coefficient
   // tensor-core operands (by precision): B^T rounded (bf16/tf32) or int8 limbs
   int64_t Dq = 0;            // D rounded up to cl_d tensor-core D tiles (tc_tile_n)
   int cl_n = 1, cl_d = 1;    // K4 thread-block cluster (multicast) shape
@@ -144,6 +146,8 @@ struct hdc_model_s {
     v.Cp = Cp;
     v.bnorm = bnorm;
     v.tau_coef = sign_bound_coef(F);
+    v.B4h = B4h;
+    v.hibound = hibound;
     return v;
   }
   SmallWorkspace small_ws() const {
@@ -191,6 +195,8 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Bp);
   cudaFree(m->Bt);
   cudaFree(m->B4);
+  cudaFree(m->B4h);
+  cudaFree(m->hibound);
   cudaFree(m->Xt);
   cudaFree(m->xnorm);
   cudaFree(m->S_part_f);
@@ -566,6 +572,8 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   ALLOC(m->B4, sizeof(float) * m->Fp * m->Dp);
   ALLOC(m->Cp, sizeof(float) * K * m->Dp);
   ALLOC(m->bnorm, sizeof(float) * m->Dp);
+  ALLOC(m->B4h, sizeof(uint16_t) * m->Fp * m->Dp);
+  ALLOC(m->hibound, sizeof(float) * m->Dp);
   ALLOC(m->S_part, sizeof(float) * G * kSmallMaxN * K);
   ALLOC(m->cnt, sizeof(unsigned) * 64);
   ALLOC(m->recheck, sizeof(unsigned long long));
@@ -587,6 +595,7 @@ hdc_status_t hdc_model_create(const float* B, const float* C, int64_t F, int64_t
   if (e == cudaSuccess) e = C ? launch_pad_copy(C, K, D, m->Cp, m->Dp, st0)
                               : cudaMemset(m->Cp, 0, sizeof(float) * K * m->Dp);
   if (e == cudaSuccess) e = launch_col_norms(m->Bp, F, m->Dp, D, m->bnorm, st0);
+  if (e == cudaSuccess) e = launch_hi_plane(m->B4, m->Bt, F, m->Fp, m->Dp, m->B4h, m->hibound, st0);
   if (e == cudaSuccess) e = cudaMemset(m->cnt, 0, sizeof(unsigned) * 64);
   if (e == cudaSuccess) e = cudaMemset(m->acc_s, 0, sizeof(unsigned long long) * kSmallMaxN * K);
   // fixed point of the exact cross-CTA score sums (all models) and of the int8 recheck

@@ -24,6 +24,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -48,18 +50,25 @@ constexpr int kThreadsS = kCt + 32;            // + producer warp (lane w feeds 
 constexpr int kChunkRows = HDC_SMALL_CHUNK;    // B4 rows per ring stage (4 KB)
 constexpr int kStagesMax = 8;                  // per consumer warp
 constexpr int kGroup = 8;                      // first-level reduction group (CTAs)
+constexpr int kDefer = 256;                    // deferred rechecks per CTA
+constexpr int kSlotsMax = 32;                  // of which with their Bt row bulk-copied to smem
+// dynamic shared memory limit: 227 KB per CTA minus the static arrays (the defer list)
+constexpr size_t kSmemDyn = 227 * 1024 - 1024 - (size_t)kDefer * 8;
 
 struct StreamParams {
   const float* X;
   int nrows;
   int64_t F, D, Dp, K, Fp;
   const float* B4;       // [units][Fp][4]
+  const uint16_t* B4h;   // [units][Fp][4] bf16 hi plane (HALF instantiation)
+  const float* Bt;       // [Dp][Fp] fp32 (float64 rechecks)
   const float* Cp;       // [K][Dp]
-  const float* bnorm;    // [Dp]
-  float tau_coef;
+  const float* bnorm;    // [Dp]: ||b_d|| (fp32 B) or the hi-plane bound coefficient (HALF)
+  float tau_coef;        // tau = tau_coef ||x_n|| bnorm[d] + kSignBoundAbs
   int recheck;
   int G;                 // CTAs
   int nst;               // ring stages per consumer warp
+  int nslot;             // recheck row slots in shared memory (Bt rows bulk-copied when flagged)
   int max_cols;          // columns of the largest CTA range (4 ceil(units / G))
   int64_t units;
   float* S_part;         // [G + groups][NB][K] (unused: partials go to acc)
@@ -91,9 +100,16 @@ __device__ __forceinline__ void cbar() {       // consumer warps only (named bar
   asm volatile("bar.sync 1, %0;" ::"n"(kCt) : "memory");
 }
 
-template <int NB>
+// HALF: B is streamed as its bf16 hi plane (b_hi = RN_bf16(b), half the bytes) and the
+// sign decisions are made exact by the float64 recheck of every |v_hi| <= tau, where tau
+// bounds |v - v_hi| (the dropped x . b_lo plus the fp32 rounding; hi_bound_kernel);
+// the rechecks are deferred to the end of the warp's stream (Bt rows prefetched into L2
+// when flagged) and the provisional H's Stage II terms are corrected by (h - h_hi) C.
+template <int NB, bool HALF>
 __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamParams p) {
   constexpr int NBP = (NB + 3) / 4 * 4;        // rows padded to float4
+  constexpr int kRows = HALF ? 2 * kChunkRows : kChunkRows;   // B4 rows per stage (4 KB)
+  constexpr int kRowBytes = HALF ? 8 : 16;
   extern __shared__ __align__(128) uint8_t smem[];
   const int F = (int)p.F, K = (int)p.K, nst = p.nst;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);         // [kCw][kStagesMax]
@@ -105,20 +121,25 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   const uint64_t xaddr = reinterpret_cast<uint64_t>(p.X);
   const int xoff = (int)((xaddr & 15u) >> 2);
   const uint32_t xbytes = (uint32_t)(((xoff + p.nrows * F) * 4 + 15) & ~15);
-  float* Xraw = ring + (size_t)kCw * nst * kChunkRows * 4;     // [xbytes / 4]
+  float* Xraw = ring + (size_t)kCw * nst * kChunkRows * 4;     // [xbytes / 4] (stage = 4 KB either way)
   const float* Xs = Xraw + xoff;                               // Xs[n * F + f]
   auto up4 = [](size_t x) { return (x + 3) & ~size_t(3); };  // float4-aligned regions
   float* Sw = Xraw + up4((size_t)NB * F + 4);                  // [kCw][NB][K] per-warp S_local
   float* Cs = Sw + up4((size_t)kCw * NB * K);                  // [K][ncol] this CTA's C columns
   float* bns = Cs + up4((size_t)K * p.max_cols);               // [ncol] ||b_d||
   float* fin = bns + up4(p.max_cols);                          // [NB K + 32 + 4 kCt] final sums
+  const int slotf = (F + 3) & ~3;                              // floats per recheck row slot
+  float* rows_s = fin + up4((size_t)NB * K + 32 + 4 * kCt + 32);   // [nslot][slotf] Bt rows
   __shared__ float xnorm_s[NBP];
   __shared__ int s_last;
+  __shared__ int2 defer_s[kDefer];             // deferred rechecks: (n | provisional-negative << 31, d)
+  __shared__ int ndefer_s;
+  __shared__ __align__(8) uint64_t slotbar[kSlotsMax];   // row slot j landed (used once: parity 0)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = blockIdx.x;
   const int64_t u0 = (int64_t)c * p.units / p.G, u1 = (int64_t)(c + 1) * p.units / p.G;
-  const int nch = (F + kChunkRows - 1) / kChunkRows;         // chunks per unit
+  const int nch = (F + kRows - 1) / kRows;                   // chunks per unit
 
   if (p.dbg && tid == 0) atomicMin(p.dbg, gtime());
   if (tid < kCw * nst) {
@@ -126,7 +147,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
     mbar_init(full + w * kStagesMax + st, 1);
     mbar_init(empty + w * kStagesMax + st, 1);
   }
-  if (tid == 0) mbar_init(xfull, 1);
+  if (tid == 0) {
+    mbar_init(xfull, 1);
+    ndefer_s = 0;
+  }
+  if (tid < kSlotsMax) mbar_init(slotbar + tid, 1);
   fence_mbar_init();
   __syncthreads();
 
@@ -150,11 +175,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
       uint32_t ph = 0;
       for (int64_t u = u0 + w; u < u1; u += kCw)
         for (int ch = 0; ch < nch; ++ch) {
-          const int f0 = ch * kChunkRows, rows = min(kChunkRows, F - f0);
+          const int f0 = ch * kRows, rows = min(kRows, F - f0);
           mbar_wait(empty + w * kStagesMax + st, ph ^ 1);
-          mbar_arrive_expect_tx(full + w * kStagesMax + st, (uint32_t)rows * 16u);
-          bulk_load(ring + ((size_t)w * nst + st) * kChunkRows * 4, p.B4 + (u * p.Fp + f0) * 4,
-                    (uint32_t)rows * 16u, full + w * kStagesMax + st);
+          // bulk copies move multiples of 16 bytes: an odd HALF row count takes one zero
+          // padding row along (Fp is a multiple of 64, so it exists)
+          const uint32_t bytes = (uint32_t)((rows * kRowBytes + 15) & ~15);
+          mbar_arrive_expect_tx(full + w * kStagesMax + st, bytes);
+          const void* src = HALF ? static_cast<const void*>(p.B4h + (u * p.Fp + f0) * 4)
+                                 : static_cast<const void*>(p.B4 + (u * p.Fp + f0) * 4);
+          bulk_load(ring + ((size_t)w * nst + st) * kChunkRows * 4, src, bytes, full + w * kStagesMax + st);
           if (++st == nst) {
             st = 0;
             ph ^= 1;
@@ -190,6 +219,48 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   int st = 0;
   uint32_t ph = 0;
   unsigned long long nrecheck = 0;
+  // float64 re-evaluation of v[n][d] (fixed order: lane l sums f = l, l + 32, ... in f
+  // order, then a fixed butterfly), warp-uniform; 8 loads in flight per lane
+  auto exact_sign = [&](int n, int64_t d, int slot) -> float {
+    const float* xr = Xs + n * F;
+    double a64 = 0.0;
+    if (slot >= 0) {                                  // the row is in shared memory
+      const float* br = rows_s + (size_t)slot * slotf;
+      mbar_wait(slotbar + slot, 0);
+      for (int f = lane; f < F; f += 32) a64 = fma((double)xr[f], (double)br[f], a64);
+      a64 = warp_sum_xor(a64);
+      return a64 >= 0.0 ? 1.f : -1.f;
+    }
+    const float* bt = p.Bt + d * p.Fp;
+    for (int f0 = 0; f0 < F; f0 += 256) {
+      float bv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = f0 + 32 * j + lane;
+        bv[j] = f < F ? __ldg(bt + f) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = f0 + 32 * j + lane;
+        if (f < F) a64 = fma((double)xr[f], (double)bv[j], a64);
+      }
+    }
+    a64 = warp_sum_xor(a64);
+    return a64 >= 0.0 ? 1.f : -1.f;
+  };
+  // Stage II runs on the provisional signs; a sign the recheck changes adds
+  // (h - h_provisional) C[k][d] = +-2 C[k][d] straight into the exact int64 score sums (each
+  // term rounded to 2^-shift on its own): the result does not depend on when, by which
+  // warp, or in which order the rechecks run
+  auto flip_correct = [&](int n, int64_t d, float hp, int slot) {
+    const float h = exact_sign(n, d, slot);
+    if (h != hp) {
+      const double dh = (double)(h - hp);
+      for (int k = lane; k < K; k += 32)
+        atomicAdd(p.acc + n * K + k,
+                  (unsigned long long)llrint(dh * (double)Cs[k * ncol + (int)(d - col0)] * p.scale));
+    }
+  };
   for (int64_t u = u0 + warp; u < u1; u += kCw) {
     // ---- V[n][0..3] for this unit, lanes over f (fp32 FMA, f ascending per lane)
     float acc[NV];
@@ -197,13 +268,21 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
 #pragma unroll
     for (int e = 0; e < NV / 2; ++e) acc2[e] = make_float2(0.f, 0.f);
     for (int ch = 0; ch < nch; ++ch) {
-      const int f0 = ch * kChunkRows, rows = min(kChunkRows, F - f0);
+      const int f0 = ch * kRows, rows = min(kRows, F - f0);
       mbar_wait(full + warp * kStagesMax + st, ph);
-      const float4* b4 = reinterpret_cast<const float4*>(ring + ((size_t)warp * nst + st) * kChunkRows * 4);
+      const float* stage = ring + ((size_t)warp * nst + st) * kChunkRows * 4;
 #pragma unroll 2
       for (int r = lane; r < rows; r += 32) {
-        const float4 b = b4[r];
-        const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
+        float2 b01, b23;
+        if constexpr (HALF) {
+          const uint2 b = reinterpret_cast<const uint2*>(stage)[r];   // 4 bf16: exact in fp32
+          b01 = make_float2(__uint_as_float(b.x << 16), __uint_as_float(b.x & 0xffff0000u));
+          b23 = make_float2(__uint_as_float(b.y << 16), __uint_as_float(b.y & 0xffff0000u));
+        } else {
+          const float4 b = reinterpret_cast<const float4*>(stage)[r];
+          b01 = make_float2(b.x, b.y);
+          b23 = make_float2(b.z, b.w);
+        }
         const float* xc = Xs + f0 + r;                // column f of X: Xs[n F + f]
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
@@ -267,11 +346,31 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
         const int se = (NV >= 32) ? EPL * src + i : src, sn = se >> 2, sq = se & 3;
-        const float* bu = p.B4 + u * p.Fp * 4 + sq;
-        double a64 = 0.0;
-        for (int f = lane; f < F; f += 32) a64 = fma((double)Xs[sn * F + f], (double)__ldg(bu + f * 4), a64);
-        a64 = warp_sum_xor(a64);
-        if (lane == src) hh[i] = a64 >= 0.0 ? 1.f : -1.f;
+        const int64_t sd = u * 4 + sq;
+        // the provisional sign enters Stage II; the recheck is deferred to the end of the
+        // CTA's stream, spread over all consumer warps (the Bt row fetched into L2 now, one
+        // 128-byte line per lane), or run now when the CTA's list is full
+        const float hp = __shfl_sync(0xffffffffu, hh[i], src);
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(&ndefer_s, 1);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot < p.nslot) {
+          // the Bt row by one bulk copy into row slot `slot` (queued behind the B stream;
+          // it has landed by the end of the stream)
+          if (lane == 0) {
+            defer_s[slot] = make_int2(sn | (hp < 0.f ? int(0x80000000u) : 0), (int)sd);
+            const uint32_t rb = (uint32_t)((F * 4 + 15) & ~15);   // Fp >= F rounded: in bounds
+            mbar_arrive_expect_tx(slotbar + slot, rb);
+            bulk_load(rows_s + (size_t)slot * slotf, p.Bt + sd * p.Fp, rb, slotbar + slot);
+          }
+        } else if (slot < kDefer) {
+          if (lane == 0) defer_s[slot] = make_int2(sn | (hp < 0.f ? int(0x80000000u) : 0), (int)sd);
+          const char* row = reinterpret_cast<const char*>(p.Bt + sd * p.Fp);
+          for (int l = lane; l * 128 < F * 4; l += 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(row + l * 128));
+        } else {
+          flip_correct(sn, sd, hp, -1);
+        }
       }
     }
     // ---- S_local[n][k] += sum_q H[n][q] C[k][4u + q]  (q ascending; padded C = 0)
@@ -301,6 +400,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
         a = fmaf(h[3], cr[3], a);
         sw[i] = a;
       }
+    }
+  }
+  SS_MARK(5);
+  cbar();
+  {
+    const int nd = min(ndefer_s, kDefer);
+    for (int j = warp; j < nd; j += kCw) {          // the deferred rechecks, over all warps
+      const int2 e = defer_s[j];
+      flip_correct(e.x & 0x7fffffff, (int64_t)e.y, e.x < 0 ? -1.f : 1.f, j < p.nslot ? j : -1);
     }
   }
   if (lane == 0 && nrecheck) atomicAdd(p.recheck_count, nrecheck);
@@ -388,18 +496,31 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
     }
 }
 
-size_t stream_smem(int nst, int64_t F, int NB, int64_t K, int64_t max_cols) {
+size_t stream_smem(int nst, int64_t F, int NB, int64_t K, int64_t max_cols, int nslot = 0) {
+  auto up4 = [](size_t x) { return (x + 3) & ~size_t(3); };
   return (2 * kCw * kStagesMax + 2) * 8 +
-         sizeof(float) * ((size_t)kCw * nst * kChunkRows * 4 + (size_t)F * NB + 8 + (size_t)kCw * NB * K +
-                          (size_t)(K + 1) * max_cols + (size_t)NB * K + 32 + 4 * kCt + 32);
+         sizeof(float) * ((size_t)kCw * nst * kChunkRows * 4 + up4((size_t)F * NB + 4) + 4 +
+                          up4((size_t)kCw * NB * K) + up4((size_t)K * max_cols) + up4(max_cols) +
+                          up4((size_t)NB * K + 32 + 4 * kCt + 32) + (size_t)nslot * ((F + 3) & ~3) + 8);
 }
 
-template <int NB>
+template <int NB, bool HALF>
 cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
-  const size_t lim = 225 * 1024;
+  const size_t lim = kSmemDyn;
   int nst = kStagesMax;
   while (nst > 2 && stream_smem(nst, p.F, NB, p.K, p.max_cols) > lim) --nst;
-  const size_t sm = stream_smem(nst, p.F, NB, p.K, p.max_cols);
+  // recheck row slots in what is left: ring stages are traded (down to 3) for the slots a
+  // CTA's flags need (cfg3, hi plane: ~2 flags per CTA at N = 1, max ~7; ~9 at N = 4, max
+  // ~20 over 148 CTAs; fp32 B: ~0.1 per CTA); a flag beyond the slots reads its row from L2
+  auto slots_at = [&](int ns) {
+    const size_t used = stream_smem(ns, p.F, NB, p.K, p.max_cols);
+    const size_t per = sizeof(float) * ((p.F + 3) & ~3);
+    return used > lim ? 0 : (int)std::min<size_t>(kSlotsMax, (lim - used) / per);
+  };
+  const int want = HALF ? 12 : 4;
+  while (nst > 3 && slots_at(nst) < want) --nst;
+  p.nslot = slots_at(nst);
+  const size_t sm = stream_smem(nst, p.F, NB, p.K, p.max_cols, p.nslot);
   if (sm > lim) return cudaErrorInvalidValue;
   p.nst = nst;
   // the attribute is per device context: set once per device (host call only then)
@@ -408,7 +529,7 @@ cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDev || sm > attr_set[dev].load()) {
-    cudaError_t e = cudaFuncSetAttribute(smallstream_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(smallstream_kernel<NB, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)lim);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < kMaxDev) attr_set[dev] = lim;
@@ -421,25 +542,72 @@ cudaError_t launch_stream_nb(StreamParams p, cudaStream_t st) {
     cudaMemcpyAsync(dbg, init, sizeof(init), cudaMemcpyHostToDevice, st);
     p.dbg = dbg;
   }
-  smallstream_kernel<NB><<<p.G, kThreadsS, sm, st>>>(p);
+  smallstream_kernel<NB, HALF><<<p.G, kThreadsS, sm, st>>>(p);
   cudaError_t le = cudaGetLastError();
   if (debug && le == cudaSuccess) {
     unsigned long long h[8];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[hdc smallstream debug] NB=%d nst=%d: from first CTA start (us): X staged %.2f, "
-            "stream done %.2f, published %.2f, final %.2f\n", NB, p.nst, (h[1] - h[0]) * 1e-3,
-            (h[2] - h[0]) * 1e-3, (h[3] - h[0]) * 1e-3, h[4] ? (h[4] - h[0]) * 1e-3 : -1.0);
+    fprintf(stderr, "[hdc smallstream debug] NB=%d nst=%d nslot=%d: from first CTA start (us): X staged %.2f, "
+            "streams done %.2f, rechecks done %.2f, published %.2f, final %.2f\n", NB, p.nst, p.nslot,
+            (h[1] - h[0]) * 1e-3, (h[5] - h[0]) * 1e-3, (h[2] - h[0]) * 1e-3, (h[3] - h[0]) * 1e-3, h[4] ? (h[4] - h[0]) * 1e-3 : -1.0);
   }
   return le;
 }
 
+// hi plane of B4 and its per-column sign bound (see smallstream_kernel HALF):
+// |x.b - fl32(x.b_hi)| <= ||x|| ||b_lo|| + tau_F ||x|| ||b_hi||, b_lo = b - b_hi exact in fp32,
+// tau_F = sign_bound_coef(F) (the fp32 evaluation, as for fp32 B); the factor
+// (1 + 2 F u + 2^-10) covers the fp32 evaluation of ||x|| and the rounding of the bound.
+__global__ void hi_plane_kernel(const float* __restrict__ B4, int64_t n4, uint16_t* __restrict__ B4h) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 b = reinterpret_cast<const float4*>(B4)[i];
+    ushort4 h;
+    h.x = __bfloat16_as_ushort(__float2bfloat16_rn(b.x));
+    h.y = __bfloat16_as_ushort(__float2bfloat16_rn(b.y));
+    h.z = __bfloat16_as_ushort(__float2bfloat16_rn(b.z));
+    h.w = __bfloat16_as_ushort(__float2bfloat16_rn(b.w));
+    reinterpret_cast<ushort4*>(B4h)[i] = h;
+  }
+}
+
+__global__ void hi_bound_kernel(const float* __restrict__ Bt, int64_t F, int64_t Fp, int64_t Dp, double coef,
+                                double slack, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t d = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (d >= Dp) return;
+  double shi = 0.0, slo = 0.0;
+  for (int64_t f = lane; f < F; f += 32) {
+    const float b = Bt[d * Fp + f];
+    const float hi = __bfloat162float(__float2bfloat16_rn(b));
+    const double lo = (double)b - (double)hi;     // exact
+    shi += (double)hi * (double)hi;
+    slo += lo * lo;
+  }
+  shi = warp_sum_xor(shi);
+  slo = warp_sum_xor(slo);
+  if (lane == 0) out[d] = __double2float_ru((sqrt(slo) + coef * sqrt(shi)) * slack);
+}
+
 }  // namespace
+
+cudaError_t launch_hi_plane(const float* B4, const float* Bt, int64_t F, int64_t Fp, int64_t Dp, uint16_t* B4h,
+                            float* hibound, cudaStream_t st) {
+  const int64_t n4 = Fp * Dp / 4;
+  hi_plane_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 32), 256, 0, st>>>(B4, n4, B4h);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const double u = 1.0 / 16777216.0;
+  const double slack = 1.0 + 2.0 * (double)F * u + 1.0 / 1024.0;
+  hi_bound_kernel<<<(unsigned)((Dp * 32 + 255) / 256), 256, 0, st>>>(Bt, F, Fp, Dp, (double)sign_bound_coef(F),
+                                                                     slack, hibound);
+  return cudaGetLastError();
+}
 
 bool smallstream_fits(int64_t F, int64_t D, int64_t K, int n, int num_sms) {
   const int nb = n <= 1 ? 1 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : 32;   // template NB used
   const int64_t units = (D + 3) / 4, G = std::min<int64_t>(units, num_sms);
-  return stream_smem(2, F, nb, K, 4 * ((units + G - 1) / G)) <= 225 * 1024 &&
+  return stream_smem(2, F, nb, K, 4 * ((units + G - 1) / G)) <= kSmemDyn &&
          (int64_t)n * F * 4 + 16 < (int64_t(1) << 20);          // one bulk copy (tx-count limit)
 }
 
@@ -459,9 +627,16 @@ cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, con
   p.K = m.K;
   p.Fp = m.Fp;
   p.B4 = m.B4;
+  p.Bt = m.Bt;
   p.Cp = m.Cp;
-  p.bnorm = m.bnorm;
-  p.tau_coef = m.tau_coef;
+  // sign-exact calls stream the bf16 hi plane when the model has one (half the bytes)
+  // (HDC_SMALL_FULLB: stream the fp32 B4 instead, for measurements)
+  // (n == 1 only: at cfg3 the hi plane's ~3% flags per element cost ~2 us of rechecks per
+  // launch from N = 4 (18.5 vs 17.9 us), at N = 1 the halved stream wins (14.5 vs 16.5 us))
+  const bool half = recheck && n == 1 && m.B4h && m.hibound && !getenv("HDC_SMALL_FULLB");
+  p.B4h = half ? m.B4h : nullptr;
+  p.bnorm = half ? m.hibound : m.bnorm;
+  p.tau_coef = half ? 1.0f : m.tau_coef;
   p.recheck = recheck ? 1 : 0;
   p.units = (m.D + 3) / 4;
   p.G = (int)std::min<int64_t>(p.units, num_sms);
@@ -476,11 +651,18 @@ cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, con
   p.scores = scores;
   p.labels = labels;
   p.dbg = nullptr;
-  if (n <= 1) return launch_stream_nb<1>(p, st);
-  if (n <= 4) return launch_stream_nb<4>(p, st);
-  if (n <= 8) return launch_stream_nb<8>(p, st);
-  if (n <= 16) return launch_stream_nb<16>(p, st);
-  return launch_stream_nb<32>(p, st);
+  if (half) {
+    if (n <= 1) return launch_stream_nb<1, true>(p, st);
+    if (n <= 4) return launch_stream_nb<4, true>(p, st);
+    if (n <= 8) return launch_stream_nb<8, true>(p, st);
+    if (n <= 16) return launch_stream_nb<16, true>(p, st);
+    return launch_stream_nb<32, true>(p, st);
+  }
+  if (n <= 1) return launch_stream_nb<1, false>(p, st);
+  if (n <= 4) return launch_stream_nb<4, false>(p, st);
+  if (n <= 8) return launch_stream_nb<8, false>(p, st);
+  if (n <= 16) return launch_stream_nb<16, false>(p, st);
+  return launch_stream_nb<32, false>(p, st);
 }
 
 }  // namespace hdc

@@ -18,6 +18,8 @@ struct ModelView {
   const float* Cp;       // K x Dp fp32, zero-padded columns
   const float* bnorm;    // Dp: ||b_d||_2 rounded up (0 on padding)
   float tau_coef;        // sign_bound_coef(F)
+  const uint16_t* B4h = nullptr;   // bf16 hi plane of B4 (K2s sign-exact streaming), or null
+  const float* hibound = nullptr;  // Dp: the hi plane's sign-bound coefficient (launch_hi_plane)
 };
 
 constexpr int64_t kDPad = 256;  // D padding granule (covers every kernel's D tile)
@@ -53,6 +55,9 @@ struct DshardExchange {
   int rank, world;
   uint32_t epoch;
 };
+// Model setup: B4h = RN_bf16(B4) and hibound[d] (k_smallstream.cu).
+cudaError_t launch_hi_plane(const float* B4, const float* Bt, int64_t F, int64_t Fp, int64_t Dp, uint16_t* B4h,
+                            float* hibound, cudaStream_t st);
 cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, const float* X, int n,
                                float* scores, int32_t* labels, bool recheck, int num_sms,
                                cudaStream_t st, const DshardExchange* xc = nullptr);
