@@ -29,9 +29,14 @@
  *     The tensor-core kernels (TF32 / BF16 / FP32_TC fused kernel, and the FP32_TC
  *     small-batch kernel) add each row's per-tile Stage II scores EXACTLY, in int64
  *     fixed point, so a row's scores and label do not depend on N, on how a batch is
- *     split into calls or shards, or on the launch configuration.  The fp32 FFMA kernels
- *     sum D-split partials in fp32 in an order that depends on N: their scores may differ
- *     in the last bits between batch sizes (labels only at near-ties).
+ *     split into calls or shards, or on the launch configuration.  The fp32 streaming
+ *     kernel (small batches) also sums its CTA partials in int64 and adds sign-recheck
+ *     corrections as integers: a row's scores do not depend on the other rows of the
+ *     batch for a given B stream (N = 1 on sign-exact models streams B's bf16 hi plane,
+ *     N >= 2 the fp32 B; the two differ in the last bits of Stage II's fp32 sums, never
+ *     in the signs).  The fp32 FFMA large-batch kernel sums D-split partials in fp32 in
+ *     an order that depends on N: its scores may differ in the last bits between batch
+ *     sizes (labels only at near-ties).
  *   - A model handle is immutable after creation but owns a workspace: calls on
  *     ONE handle must be serialised (one stream at a time); use one handle per
  *     concurrent stream.

@@ -200,6 +200,54 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   const int64_t col0 = u0 * 4;
   float* sw = Sw + (size_t)warp * NB * K;
   for (int i = lane; i < NB * K; i += 32) sw[i] = 0.f;
+  // float64 re-evaluation of v[n][d] (fixed order: lane l sums f = l, l + 32, ... in f
+  // order, then a fixed butterfly), warp-uniform; 8 loads in flight per lane
+  auto dot_smem = [&](const float* xr, const float* br) -> double {
+    double a64 = 0.0;
+    for (int f = lane; f < F; f += 32) a64 = fma((double)xr[f], (double)br[f], a64);
+    return warp_sum_xor(a64);
+  };
+  auto dot_global = [&](const float* xr, const float* bt) -> double {
+    double a64 = 0.0;
+    for (int f0 = 0; f0 < F; f0 += 256) {
+      float bv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = f0 + 32 * j + lane;
+        bv[j] = f < F ? __ldg(bt + f) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int f = f0 + 32 * j + lane;
+        if (f < F) a64 = fma((double)xr[f], (double)bv[j], a64);
+      }
+    }
+    return warp_sum_xor(a64);
+  };
+  auto exact_sign = [&](int n, int64_t d, int slot) -> float {
+    const float* xr = Xs + n * F;
+    double a64;
+    if (slot >= 0) {                                  // the row is in shared memory
+      mbar_wait(slotbar + slot, 0);
+      a64 = dot_smem(xr, rows_s + (size_t)slot * slotf);
+    } else {
+      a64 = dot_global(xr, p.Bt + d * p.Fp);
+    }
+    return a64 >= 0.0 ? 1.f : -1.f;
+  };
+  // Stage II runs on the provisional signs; a sign the recheck changes adds
+  // (h - h_provisional) C[k][d] = +-2 C[k][d] straight into the exact int64 score sums (each
+  // term rounded to 2^-shift on its own): the result does not depend on when, by which
+  // warp, or in which order the rechecks run
+  auto flip_correct = [&](int n, int64_t d, float hp, int slot) {
+    const float h = exact_sign(n, d, slot);
+    if (h != hp) {
+      const double dh = (double)(h - hp);
+      for (int k = lane; k < K; k += 32)
+        atomicAdd(p.acc + n * K + k,
+                  (unsigned long long)llrint(dh * (double)Cs[k * ncol + (int)(d - col0)] * p.scale));
+    }
+  };
   cbar();
   mbar_wait(xfull, 0);
   // zero rows nrows..NB-1 (also overwrites the bulk copy's tail slack past row nrows-1)
@@ -219,48 +267,6 @@ __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamP
   int st = 0;
   uint32_t ph = 0;
   unsigned long long nrecheck = 0;
-  // float64 re-evaluation of v[n][d] (fixed order: lane l sums f = l, l + 32, ... in f
-  // order, then a fixed butterfly), warp-uniform; 8 loads in flight per lane
-  auto exact_sign = [&](int n, int64_t d, int slot) -> float {
-    const float* xr = Xs + n * F;
-    double a64 = 0.0;
-    if (slot >= 0) {                                  // the row is in shared memory
-      const float* br = rows_s + (size_t)slot * slotf;
-      mbar_wait(slotbar + slot, 0);
-      for (int f = lane; f < F; f += 32) a64 = fma((double)xr[f], (double)br[f], a64);
-      a64 = warp_sum_xor(a64);
-      return a64 >= 0.0 ? 1.f : -1.f;
-    }
-    const float* bt = p.Bt + d * p.Fp;
-    for (int f0 = 0; f0 < F; f0 += 256) {
-      float bv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int f = f0 + 32 * j + lane;
-        bv[j] = f < F ? __ldg(bt + f) : 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int f = f0 + 32 * j + lane;
-        if (f < F) a64 = fma((double)xr[f], (double)bv[j], a64);
-      }
-    }
-    a64 = warp_sum_xor(a64);
-    return a64 >= 0.0 ? 1.f : -1.f;
-  };
-  // Stage II runs on the provisional signs; a sign the recheck changes adds
-  // (h - h_provisional) C[k][d] = +-2 C[k][d] straight into the exact int64 score sums (each
-  // term rounded to 2^-shift on its own): the result does not depend on when, by which
-  // warp, or in which order the rechecks run
-  auto flip_correct = [&](int n, int64_t d, float hp, int slot) {
-    const float h = exact_sign(n, d, slot);
-    if (h != hp) {
-      const double dh = (double)(h - hp);
-      for (int k = lane; k < K; k += 32)
-        atomicAdd(p.acc + n * K + k,
-                  (unsigned long long)llrint(dh * (double)Cs[k * ncol + (int)(d - col0)] * p.scale));
-    }
-  };
   for (int64_t u = u0 + warp; u < u1; u += kCw) {
     // ---- V[n][0..3] for this unit, lanes over f (fp32 FMA, f ascending per lane)
     float acc[NV];
@@ -633,7 +639,9 @@ cudaError_t launch_smallstream(const ModelView& m, const SmallWorkspace& ws, con
   // (HDC_SMALL_FULLB: stream the fp32 B4 instead, for measurements)
   // (n == 1 only: at cfg3 the hi plane's ~3% flags per element cost ~2 us of rechecks per
   // launch from N = 4 (18.5 vs 17.9 us), at N = 1 the halved stream wins (14.5 vs 16.5 us))
-  const bool half = recheck && n == 1 && m.B4h && m.hibound && !getenv("HDC_SMALL_FULLB");
+  // (HDC_SMALL_HALF4: also at 2 <= n <= 4, a measurement switch)
+  const bool half = recheck && (n == 1 || (n <= 4 && getenv("HDC_SMALL_HALF4"))) && m.B4h && m.hibound &&
+                    !getenv("HDC_SMALL_FULLB");
   p.B4h = half ? m.B4h : nullptr;
   p.bnorm = half ? m.hibound : m.bnorm;
   p.tau_coef = half ? 1.0f : m.tau_coef;
