@@ -54,7 +54,7 @@ def test_cfg3_hi_plane_vs_oracle(hdc, name):
     assert np.array_equal(y, orc["y"])
     yf, Sf, nf = _run(m, X, fullb=True)
     check_fp32(orc, yf, Sf)
-    # the hi plane (N = 1) has a bound ~2^-9 ||b_lo|| / ||b|| wider: many more rechecks,
+    # the hi plane (N = 1) has a bound ~||b_lo|| / (tau_F ||b||) ~ 10^3 times wider: many more rechecks,
     # same signs; from 2 rows K2s streams the fp32 B
     if cfg.N == 1:
         assert nh > 4 * nf
