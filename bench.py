@@ -184,6 +184,37 @@ def measured_traffic(cfg_name, prec):
     return best
 
 
+def gpu_local_cpus(dev_index):
+    """CPUs of the GPU's NUMA node (sysfs local_cpulist of its PCI function), or None."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(dev_index)
+        bus = "%04x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        with open("/sys/bus/pci/devices/%s/local_cpulist" % bus) as f:
+            txt = f.read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
+def pinned_local(make, dev_index):
+    """Allocate pinned host memory from a thread on the GPU's NUMA node (first touch there),
+    so host->device copies do not cross the socket link; the process affinity is restored."""
+    cpus = gpu_local_cpus(dev_index)
+    old = os.sched_getaffinity(0)
+    try:
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return make(), (sorted(cpus) if cpus else None)
+    finally:
+        os.sched_setaffinity(0, old)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
     from hdc_inputs import CONFIGS, make_B, make_C, make_X
@@ -517,8 +548,9 @@ def run_ours(args, rank, world, local_rank):
     # end to end through the public host-buffer entry point (H2D X, D2H labels)
     e2e = None
     if not args.no_e2e and not args.dshard and args.mode == "infer":
-        Xh = X.cpu().pin_memory()
-        yh = torch.empty(n_local, dtype=torch.int32).pin_memory()
+        (Xh, yh), local = pinned_local(lambda: (X.cpu().pin_memory(),
+                                                torch.empty(n_local, dtype=torch.int32).pin_memory()),
+                                       local_rank)
         # warm the host path to steady state: the first tens of back-to-back calls run up
         # to 3x slower while the host-device link ramps up (measured: 2.1 -> 0.74 ms per
         # cfg2 call over ~20 calls), so warm up for >= 30 calls and >= 0.2 s
@@ -546,6 +578,8 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(Xh.numel() * 4) * (world if strong else 1),
                "d2h_bytes_per_step": int(yh.numel() * 4) * (world if strong else 1),
                "api": "hdc_model_infer_host (pinned host X -> labels in mapped pinned host memory)",
+               "host_numa": ("pinned buffers first-touched on the GPU's NUMA node (%d local CPUs, "
+                             "sysfs local_cpulist)" % len(local)) if local else "no NUMA information",
                "gather": "none: each rank's labels land in its own host memory" if world > 1 else None}
 
     # one-shot hdc_infer (model creation inside the call), reported separately
