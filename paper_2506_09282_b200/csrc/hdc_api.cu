@@ -98,6 +98,7 @@ struct hdc_model_s {
   void* Atc = nullptr;       // [NL][Np][Fp]
   int64_t* rowtau = nullptr; // [Np]
   long long* S_part_tc = nullptr;
+  long long* S_acc_tc = nullptr;      // [tw_rows][Kp] K4's red.add sums of many-partial N-tiles
   unsigned* cnt_tc = nullptr;
   float* Cp = nullptr;
   float* bnorm = nullptr;
@@ -186,6 +187,7 @@ void free_model_memory(hdc_model_s* m) {
   cudaFree(m->Atc);
   cudaFree(m->rowtau);
   cudaFree(m->S_part_tc);
+  cudaFree(m->S_acc_tc);
   cudaFree(m->cnt_tc);
   cudaFree(m->flags);
   cudaFree(m->flag_count);
@@ -281,19 +283,22 @@ hdc_status_t ensure_tc_ws(hdc_model_s* m, int64_t N) {
   cudaFree(m->Atc);
   cudaFree(m->rowtau);
   cudaFree(m->S_part_tc);
+  cudaFree(m->S_acc_tc);
   cudaFree(m->cnt_tc);
   cudaFree(m->flags);
   cudaFree(m->flag_count);
   cudaFree(m->corr);
   cudaFree(m->dirty);
   cudaFree(m->S_ws);
-  m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->cnt_tc = nullptr;
+  m->Atc = nullptr; m->rowtau = nullptr; m->S_part_tc = nullptr; m->S_acc_tc = nullptr; m->cnt_tc = nullptr;
   m->flags = nullptr; m->flag_count = nullptr; m->corr = nullptr; m->dirty = nullptr; m->S_ws = nullptr;
   m->tw_rows = 0;
   m->tw_slots = 0;
   cudaError_t e = cudaMalloc(&m->Atc, tc_esz(mode) * tc_limbs(mode) * rows * m->Fp);
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->rowtau, sizeof(int64_t) * rows);
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_part_tc, sizeof(long long) * nsl * kTileM * tc_kp(m->K));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&m->S_acc_tc, sizeof(long long) * rows * tc_kp(m->K));
+  if (e == cudaSuccess) e = cudaMemset(m->S_acc_tc, 0, sizeof(long long) * rows * tc_kp(m->K));
   if (e == cudaSuccess) e = cudaMalloc((void**)&m->cnt_tc, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess) e = cudaMemset(m->cnt_tc, 0, sizeof(unsigned) * (rows / kTileM));
   if (e == cudaSuccess && mode >= 2) {
@@ -372,6 +377,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.coltau_m = m->coltau_m;
   o.flag_shift = tc_flag_shift(m->Fp);
   o.S_part = m->S_part_tc;
+  o.S_acc = m->S_acc_tc;
   o.s_part_slots = m->tw_slots;
   o.shift = m->corr_shift;
   o.cnt = m->cnt_tc;

@@ -170,6 +170,7 @@ struct TcParams {
   const uint8_t* Cil;      // per D-tile Stage II operand (see Cfg::C_SLOT), c_tile_bytes each
   uint32_t c_tile_bytes;
   long long* S_part;       // [CTAs][nslot][BM][Kp] int64 fixed-point partial scores of split N-tiles
+  long long* S_acc;        // [N_p][Kp] int64 sums of N-tiles split over > 8 CTAs (red.add), zero between calls
   double scale, inv_scale; // 2^shift, 2^-shift: the fixed point of the Stage II sums (tc_corr_shift)
   float scale_f;           // 2^shift as a normal float, else 0 (then the fp64 conversion)
   int64_t s_part_cap;      // capacity of S_part in [BM][K] slots
@@ -1025,7 +1026,21 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         continue;
       }
       const int myslot = (CLD == 1) ? ((ng == first_ng) ? 0 : 1) : (ng - first_ng);
-      {
+      const int P = (c_last - c_first + 1) * CLD;     // partials per row of this N-tile
+      // many partials (small N: the N-tile's D-range spread over many clusters): every
+      // contributor adds its exact sums into the N-tile's int64 accumulator (red.add, spread
+      // over the rows' L2 lines) instead of a partial slot, so the last arriver reads one sum
+      // per (row, class) instead of P partials
+      const bool many = P > 8 && p.S_acc != nullptr;
+      if (many) {
+#pragma unroll
+        for (int u = 0; u < KQ_MAX; ++u) {
+          if (u < kq && row_ok && kq0 + u < K)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.S_acc + row * p.Kp + kq0 + u),
+                      (unsigned long long)sacc[u]);
+          sacc[u] = 0;
+        }
+      } else {
         long long* part = p.S_part + (((int64_t)c * p.nslot + myslot) * BM + m) * p.Kp + kq0;
 #pragma unroll
         for (int u = 0; u < KQ_MAX; ++u) {
@@ -1041,7 +1056,6 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (*s_flag) p.cnt[ni] = 0u;
       }
       named_bar(1, NUM_EPI * 32);
-      const int P = (c_last - c_first + 1) * CLD;     // partials per row of this N-tile
       // slot of this N-tile in a contributing CTA's S_part: clusters after c_first start
       // inside N-group ng (slot 0); c_first may have started in an earlier one
       const int ng_first = (int)(range_begin(c_first, p.T, p.G, p.runit) / p.TdG);
@@ -1054,7 +1068,34 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int64_t r0 = (int64_t)ni * BM;
       const int nv = (int)((p.N - r0) < BM ? (p.N - r0) : BM);
       const int pairs = nv > 0 ? nv * K : 0;          // (row, class) sums of this N-tile
-      if (*s_flag && P > 8) {
+      if (*s_flag && many) {
+        // the N-tile's sums are complete in S_acc: read and reset them (for the next call),
+        // scores to p.scores (always non-null here), then one thread per row takes the argmax
+        __threadfence();
+        if (row_ok) {
+#pragma unroll
+          for (int u = 0; u < KQ_MAX; ++u) {
+            const int k = kq0 + u;
+            if (u < kq && k < K) {
+              const long long v = (long long)atomicExch(reinterpret_cast<unsigned long long*>(p.S_acc + row * p.Kp + k), 0ull);
+              p.scores[row * p.K + k] = (float)((double)v * p.inv_scale);
+            }
+          }
+        }
+        named_bar(1, NUM_EPI * 32);
+        if (cq == 0 && row_ok) {
+          int best = 0;
+          float bv = 0.f;
+          for (int k = 0; k < K; ++k) {
+            const float v = p.scores[row * p.K + k];
+            if (k == 0 || v > bv) {
+              bv = v;
+              best = k;
+            }
+          }
+          if (p.labels) p.labels[row] = best;
+        }
+      } else if (*s_flag && P > 8) {
         // Many partials (small N: the N-tile's D-range is spread over many clusters). The
         // sums go to p.scores (always non-null here), then one thread per row takes the
         // argmax.  Few pairs: a warp per pair, lanes splitting the partials; otherwise a
@@ -1735,6 +1776,7 @@ cudaError_t launch_fused_tc(int mode, const TcOperands& o, int64_t N, float* sco
   p.Cil = (const uint8_t*)o.Cil;
   p.c_tile_bytes = (uint32_t)tc_c_tile_bytes(mode, o.K);
   p.S_part = o.S_part;
+  p.S_acc = o.S_acc;
   p.s_part_cap = o.s_part_slots;
   p.scale = ldexp(1.0, o.shift);
   p.inv_scale = ldexp(1.0, -o.shift);

@@ -95,6 +95,7 @@ struct TcOperands {
   const int32_t* coltau_m;           // [Dq]  int8 mode: ceil(coltau / 2^flag_shift) (tc_flag_shift)
   int flag_shift;
   long long* S_part;                 // [s_part_slots][128][Kp] int64 fixed-point partial scores
+  long long* S_acc = nullptr;        // [N_p][Kp] int64 sums of N-tiles split over > 8 CTAs, zero between calls
   int64_t s_part_slots;
   int shift;                         // fixed-point shift of the Stage II sums (tc_corr_shift)
   unsigned* cnt;                     // [N_p / 128]
