@@ -57,6 +57,7 @@ constexpr int kSmallMaxNLowp = 8;          // bf16 / tf32 models (see run())
 constexpr int64_t kWideMinFp = 768;        // int8 wide K4 from this padded F (tools/gpu/r2_wsweep.py:
                                            // wide/80-column time 1.0-1.02 at F = 640, 0.93-0.95 at 784)
 constexpr int kSmallTcMinN = 5;            // fp32_tc models: K2t from this many rows (see run())
+constexpr int64_t kInlineRecheckElems = 4000000;   // int8 K4: in-kernel rechecks up to N x Dq (run_fused_tc)
 constexpr int kHostChunksMax = 8;        // chunks of the pipelined host-buffer path
 
 }  // namespace
@@ -385,7 +386,12 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   o.Cp = m->Cp;
   o.flags = m->flags;
   o.flag_count = m->flag_count;
-  o.flag_cap = m->flag_cap;
+  // int8 mode, small batches (N x Dq <= kInlineRecheckElems, cfg1: ~1 flag per CTA): the
+  // fused kernel re-evaluates its flags itself and the recheck / finalize launches are
+  // skipped; HDC_TC_INLINE_RECHECK=0/1 overrides (measurements)
+  const char* irc = getenv("HDC_TC_INLINE_RECHECK");
+  const bool inline_rc = mode >= 2 && (irc ? atoi(irc) != 0 : N * m->Dq <= kInlineRecheckElems);
+  o.flag_cap = inline_rc ? 0 : m->flag_cap;
   o.corr = m->corr;
   o.dirty = m->dirty;
   o.hout = m->hout;
@@ -399,7 +405,7 @@ hdc_status_t run_fused_tc(hdc_model_s* m, const float* X, int64_t N, int32_t* la
   if (e != cudaSuccess) return cuda_fail(e, "fused_tc launch");
   m->last_launches = 2;
   m->last_kernel = HDC_KERNEL_TC;
-  if (mode >= 2) {
+  if (mode >= 2 && !inline_rc) {
     e = launch_tc_recheck(o, N, S, labels, m->corr_shift, st);
     if (e != cudaSuccess) return cuda_fail(e, "tc recheck launch");
     m->last_launches = 4;

@@ -877,7 +877,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // ---- phase 2 (int8 mode): flagged signs are appended to a global list with the
       // provisional sign used in H; hdc_recheck_kernel re-evaluates them in float64 after
       // this kernel and corrects S exactly where a sign flips (Stage II is linear in H).
-      // Only a list overflow (e.g. many all-zero rows) falls back to re-evaluating here.
+      // Only a list overflow (e.g. many all-zero rows) falls back to re-evaluating here, and
+      // small batches (no list: flag_cap == 0), whose ~1 flag per CTA costs less than the two
+      // extra launches.
       if constexpr (I8) {
 #pragma unroll
         for (int w = 0; w < NWB; ++w) {
@@ -887,7 +889,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int bit = __ffs(fw) - 1;
             fw &= fw - 1;
             const int col = cq * EPI_COLS + w * 32 + bit;
-            const unsigned long long slot = atomicAdd(p.flag_count, 1ull);
+            // flag_cap == 0: small batches re-evaluate every flag here (no list, no
+            // recheck / finalize launches)
+            const unsigned long long slot = p.flag_cap ? atomicAdd(p.flag_count, 1ull) : ~0ull;
             if (slot < p.flag_cap) {
               const uint32_t neg = (hbits[w] >> bit) & 1u;
               p.flags[slot] = make_uint2((uint32_t)row, (uint32_t)((int64_t)di * BN + col) | (neg << 31));

@@ -56,6 +56,38 @@ def test_tc_exact_cancellations_and_zero_rows(hdc):
     m.close()
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cancel"])
+def test_tc_inline_recheck_matches_list(hdc, monkeypatch, case):
+    """Small batches re-evaluate K4's flagged signs inside the kernel (no list, no recheck /
+    finalize launches); larger ones append them to the list for tc_recheck_kernel.  Both
+    must meet the fp32 policy and agree on every label (scores to Stage II rounding)."""
+    if case == "cfg1":
+        cfg = CONFIGS["cfg1"]
+        X, B, C = make_X(cfg), make_B(cfg), make_C(cfg)
+    else:
+        rng = np.random.default_rng(12)
+        X = rng.integers(-2, 3, (200, 6)).astype(np.float32)
+        X[3] = 0.0
+        B = rng.integers(-2, 3, (6, 900)).astype(np.float32)
+        C = rng.standard_normal((5, 900)).astype(np.float32)
+    orc = oracle.infer(X, B, C, allow=True, nthreads=0)
+    Bd, Cd = to_dev(B, C)
+    m = hdc.Model(Bd, Cd, prec="fp32_tc")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("HDC_TC_INLINE_RECHECK", mode)
+        n0 = m.recheck_count()
+        y, S = run_model(m, X, path="fused")
+        assert m.last_kernel() == "tc" and m.last_launch_count() == (2 if mode == "1" else 4)
+        rep = check_fp32(orc, y, S)
+        assert rep["score_violations"] == 0
+        out[mode] = (y, S, m.recheck_count() - n0)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=0, atol=1e-6 * np.abs(C).sum(1).max())
+    assert out["1"][2] == out["0"][2]               # the same flags, re-evaluated either way
+    m.close()
+
+
 def test_tc_int8_matches_ffma_labels(hdc, monkeypatch):
     cfg = CONFIGS["cfg1"]
     X, B, C = make_X(cfg), make_B(cfg), make_C(cfg)
