@@ -7,18 +7,19 @@
 // paper's ScalableHD-S (Alg. 3): D is split into one contiguous range of
 // 4-column units per CTA (148 CTAs); each CTA forms complete F-sums for its columns
 // (HardSign needs all of F), applies HardSign and contracts with its C columns into
-// a partial S (the paper's S_local); the partials are summed in a fixed order (the
-// paper's `S += S_local`) by a two-level last-arriver reduction.
+// a partial S (the paper's S_local); the partials are summed (the paper's `S += S_local`,
+// P:336) in int64 fixed point by atomics -- exact, so order-free -- and the last-arriving
+// CTA converts them and takes the argmax.
 //
 // B200 mapping.  The model keeps B unit-major (B4[u][f][4]: all F rows of a 4-column
 // unit contiguous), so a CTA's share of B is one contiguous run of HBM.  A producer
-// warp streams it with 1-D TMA bulk copies (cp.async.bulk, 8 KB chunks) through a
-// shared-memory ring of up to 12 stages (96 KB in flight per SM: enough bytes in
-// flight to cover HBM latency at 1/148 of the chip's bandwidth), started before X is
-// staged; 10 consumer warps run the FFMA contraction from shared memory.
+// warp streams it with 1-D TMA bulk copies (cp.async.bulk, 4 KB chunks) through
+// per-consumer-warp shared-memory rings (3-5 stages each, ~160-200 KB in flight per SM),
+// started before X is staged; 10 consumer warps run the FFMA contraction from shared
+// memory.  Sign-exact N = 1 streams the bf16 hi plane of B instead (half the bytes).
 //
-// HDC_PREC_FP32 sign exactness: |v| <= tau = c_F ||x_n|| ||b_d|| is re-evaluated in
-// float64 (warp-cooperative, fixed order), as in the other fp32 kernels.
+// Sign exactness (fp32 semantics): |v| <= tau (c_F ||x_n|| ||b_d||, or the hi plane's
+// bound) is re-evaluated in float64 (warp-cooperative, fixed order) after the stream.
 #include <atomic>
 #include <algorithm>
 #include <cstdio>
@@ -60,7 +61,7 @@ struct StreamParams {
   int nrows;
   int64_t F, D, Dp, K, Fp;
   const float* B4;       // [units][Fp][4]
-  const uint16_t* B4h;   // [units][Fp][4] bf16 hi plane (HALF instantiation)
+  const uint16_t* B4h;   // [units][Fp][4] bf16 hi plane (HALF instantiation; N = 1 sign-exact)
   const float* Bt;       // [Dp][Fp] fp32 (float64 rechecks)
   const float* Cp;       // [K][Dp]
   const float* bnorm;    // [Dp]: ||b_d|| (fp32 B) or the hi-plane bound coefficient (HALF)
@@ -102,9 +103,11 @@ __device__ __forceinline__ void cbar() {       // consumer warps only (named bar
 
 // HALF: B is streamed as its bf16 hi plane (b_hi = RN_bf16(b), half the bytes) and the
 // sign decisions are made exact by the float64 recheck of every |v_hi| <= tau, where tau
-// bounds |v - v_hi| (the dropped x . b_lo plus the fp32 rounding; hi_bound_kernel);
-// the rechecks are deferred to the end of the warp's stream (Bt rows prefetched into L2
-// when flagged) and the provisional H's Stage II terms are corrected by (h - h_hi) C.
+// bounds |v - v_hi| (the dropped x . b_lo plus the fp32 rounding; hi_bound_kernel).
+// Both instantiations defer their rechecks to the end of the CTA's stream: a flagged sign's
+// fp32 B^T row is bulk-copied into a shared-memory slot (or prefetched into L2 past the
+// slots), Stage II runs on the provisional sign, and a sign the float64 dot changes adds
+// (h - h_provisional) C[k][d] to the exact int64 score sums.
 template <int NB, bool HALF>
 __global__ void __launch_bounds__(kThreadsS, 1) smallstream_kernel(const StreamParams p) {
   constexpr int NBP = (NB + 3) / 4 * 4;        // rows padded to float4
