@@ -308,9 +308,9 @@ def roofline_for(cfg, prec, path, ms_kernel, peaks, run_peaks, units, kernel=Non
         out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                "frac": achieved / peak, "traffic": None, "algorithmic_per_launch": bytes_,
                "algorithmic_unit": "bytes: 4 D (F + K) + 4 N F + 4 N (B, C once; X; labels)"}
-        if kernel == "small" and prec in ("fp32", "fp32_tc") and not os.environ.get("HDC_SMALL_FULLB"):
-            # sign-exact K2s streams B as its bf16 hi plane (DESIGN §2 K2s): half of B's
-            # algorithmic bytes cross HBM, plus the fp32 B^T rows of the rechecked columns
+        if kernel == "small" and N == 1 and prec in ("fp32", "fp32_tc") and not os.environ.get("HDC_SMALL_FULLB"):
+            # sign-exact K2s at N = 1 streams B as its bf16 hi plane (DESIGN §2 K2s): half of
+            # B's algorithmic bytes cross HBM, plus the fp32 B^T rows of the rechecked columns
             streamed = 2.0 * D * F + 4.0 * D * K + 4.0 * N * F + 4.0 * N
             out.update(b_stream="bf16 hi plane (2 B per element) + fp32 B^T rows of rechecked columns",
                        streamed_min_per_launch=streamed,
